@@ -1,0 +1,169 @@
+/*
+ * ente_b200.h -- C ABI of the B200-native ensemble-TE hot path.
+ *
+ * The reference (`ente`, /root/reference/pkg/src/ente) is pure Python with no
+ * FFI; its boundary is the Python functions listed beside each entry point.
+ * These entry points are what a ctypes binding of that boundary calls (see
+ * INTEGRATION.md).  Conventions:
+ *
+ *   - every array argument marked [dev] is a DEVICE pointer owned by the
+ *     caller; [host] arrays are read before the call returns;
+ *   - every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and does not synchronise unless stated;
+ *   - scratch memory comes from the caller through (workspace, ws_bytes),
+ *     sized by the matching *_workspace_size() call;
+ *   - the return value is ENTE_OK or a negative ente_status; the message of
+ *     the last failure on the calling thread is ente_last_error();
+ *   - per-chunk outcomes are reported in status[] (ente_chunk_status) and are
+ *     mapped by the host onto the reference exception types
+ *     (exceptions.py: ShapeMismatch, KTooLarge, DegenerateData).
+ *
+ * Point matrices are row-major [rows x dim] fp64 exactly as numpy lays out
+ * a C-contiguous `Chunk.points` (engine.py:53-59); chunk c owns rows
+ * [row0, row0 + n).
+ */
+#ifndef ENTE_B200_H
+#define ENTE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ENTE_OK = 0,
+    ENTE_ERR_ARG = -1,      /* invalid argument (shape, k, dim, ...) */
+    ENTE_ERR_CUDA = -2,     /* a CUDA runtime call failed */
+    ENTE_ERR_WORKSPACE = -3 /* workspace smaller than *_workspace_size() */
+} ente_status;
+
+typedef enum {
+    ENTE_CHUNK_OK = 0,
+    ENTE_CHUNK_K_TOO_LARGE = 1, /* KTooLarge: k not in [1, n-1] (engine.py:173-174) */
+    ENTE_CHUNK_NONFINITE = 2,   /* ShapeMismatch: non-finite values (engine.py:57-58) */
+    ENTE_CHUNK_DEGENERATE = 3   /* DegenerateData: ptp == 0 in every column (ksg.py:80-81) */
+} ente_chunk_status;
+
+/* One search problem: rows [row0, row0 + n) of the batch point matrix. */
+typedef struct {
+    int64_t row0;
+    int32_t n;
+    int32_t reserved;
+} ente_chunk;
+
+/* Library version string and the CUDA arch it was built for. */
+const char *ente_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+const char *ente_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * ente_search -- exact k-th nearest-neighbour max-norm distances and strict
+ * marginal radius counts for a batch of chunks sharing `dim`.
+ *
+ * Replaces: ente.engine.batch_search          engine.py:203-216
+ *           (knn_kth_distances engine.py:170-176, radius_counts 179-188,
+ *            _search_one 191-200)
+ *
+ *   pts64        [dev]  [total_rows x dim] fp64, row-major
+ *   chunks       [host] n_chunks descriptors
+ *   marg_masks   [host] n_marg column bitmasks (bit c = column c), 1..8
+ *                       masks, dim <= 32; a marginal is the max-norm over
+ *                       its columns (engine.py:194-199)
+ *   k                   neighbour order, 1 <= k <= n-1 for every chunk
+ *   out_eps      [dev]  [total_rows] fp64 kth_distance, bit-identical to the
+ *                       reference's fp64 sweep
+ *   out_counts   [dev]  [n_marg x total_rows] int32 strict counts
+ *   status       [dev]  [n_chunks] int32 ente_chunk_status
+ *
+ * Chunks with status != OK have undefined outputs.
+ * ------------------------------------------------------------------------- */
+size_t ente_search_workspace_size(const ente_chunk *chunks, int n_chunks, int dim, int n_marg,
+                                  int k);
+int ente_search(const double *pts64, int64_t total_rows, int dim, const ente_chunk *chunks,
+               int n_chunks, const uint32_t *marg_masks, int n_marg, int k, double *out_eps,
+               int32_t *out_counts, int32_t *status, void *workspace, size_t ws_bytes,
+               void *stream);
+
+/* ---------------------------------------------------------------------------
+ * ente_radius_counts -- strict counts #{j != i : maxnorm_marg(p_i, p_j) < r_i}
+ * for caller-given radii (fp64, exact), one count array per marginal.
+ *
+ * Replaces: ente.engine.radius_counts         engine.py:179-188
+ *
+ *   radii        [dev]  [total_rows] fp64, >= 0 (the host raises ShapeMismatch
+ *                       for negative radii, engine.py:185-186)
+ *   out_counts   [dev]  [n_marg x total_rows] int32
+ * ------------------------------------------------------------------------- */
+size_t ente_radius_counts_workspace_size(int n_chunks);
+int ente_radius_counts(const double *pts64, int64_t total_rows, int dim, const ente_chunk *chunks,
+                       int n_chunks, const uint32_t *marg_masks, int n_marg, const double *radii,
+                       int32_t *out_counts, int32_t *status, void *workspace, size_t ws_bytes,
+                       void *stream);
+
+/* ---------------------------------------------------------------------------
+ * ente_jitter -- tie-breaking jitter, in place:
+ *   pts += U(-1, 1) * (amplitude * std(pts, axis=0))     per chunk
+ * with numpy's exact arithmetic: column std as a sequential row-order sum
+ * (mean, squared deviations, /n, sqrt), U(-1,1) = -1 + 2 * ((raw >> 11) * 2^-53)
+ * from the chunk's PCG64 stream in C order (element r*dim + c).  Also flags
+ * degenerate chunks (ptp == 0 in every column after jitter, ksg.py:80-81)
+ * and non-finite values (engine.py:57-58) in status.
+ *
+ * Replaces: ente.ksg._jittered_joint          ksg.py:52-59
+ *
+ *   pcg_state    [host] n_chunks x 4 uint64: {state_hi, state_lo, inc_hi,
+ *                       inc_lo} = np.random.PCG64(seed).state before any draw
+ *   amplitude           jitter amplitude; <= 0 skips the jitter but still
+ *                       runs the checks
+ * ------------------------------------------------------------------------- */
+int ente_jitter(double *pts64, int dim, const ente_chunk *chunks, int n_chunks,
+                const uint64_t *pcg_state, double amplitude, int32_t *status, void *workspace,
+                size_t ws_bytes, void *stream);
+size_t ente_jitter_workspace_size(int n_chunks, int dim);
+
+/* ---------------------------------------------------------------------------
+ * ente_pack_te -- build the joint point matrix of every (u, surrogate) chunk
+ * of an analyze_pair call directly from the two ensembles:
+ *   joint row (r, t') = [ y(phi(r), t') | y-past(phi(r), t'-1) | x-past(r, t'-u) ]
+ * rows repetition-outer / time-inner, phi = identity for originals.
+ *
+ * Replaces: ente.embedding.assemble_pointsets  embedding.py:75-120
+ *           ente.inference._permuted_bundle    inference.py:105-117
+ *
+ *   x, y         [dev]  [reps x n_samples] fp64 source / target ensembles
+ *   items        [host] n_items x 2 int32: {u, perm_index (-1 = original)}
+ *   perms        [dev]  [n_perm x reps] int32 repetition permutations
+ *   out          [dev]  [n_items * reps * w x (1 + dy + dx)] fp64
+ * Window t_lo..t_hi is 1-based inclusive; callers validate IndexUnderflow.
+ * ------------------------------------------------------------------------- */
+int ente_pack_te(const double *x, const double *y, int reps, int n_samples, int dx, int tau_x,
+                 int dy, int tau_y, int t_lo, int t_hi, const int32_t *items, int n_items,
+                 const int32_t *perms, double *out, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * ente_te_reduce -- KSG transfer entropy of each TE-layout chunk:
+ *   te = psi(k) + mean(sort(psi(a+1) - psi(b+1) - psi(c+1)))
+ * with numpy's exact order: bracket evaluated left to right, ascending sort,
+ * numpy pairwise summation (blocks of 8, PW_BLOCKSIZE 128), division by n.
+ *
+ * Replaces: ente.ksg.te_from_counts           ksg.py:39-49
+ *
+ *   counts       [dev]  [3 x total_rows] int32: n_ypast, n_y_ypast,
+ *                       n_ypast_xpast (the layout ente_search writes for the
+ *                       marginal masks of PointSetBundle, embedding.py:50-60)
+ *   psi_table    [dev]  psi(m + 1) for m = 0 .. table_len-1 (scipy values)
+ *   psi_k               psi(k)
+ *   out_te       [dev]  [n_chunks] fp64
+ * ------------------------------------------------------------------------- */
+size_t ente_te_reduce_workspace_size(const ente_chunk *chunks, int n_chunks);
+int ente_te_reduce(const int32_t *counts, int64_t total_rows, const ente_chunk *chunks,
+                   int n_chunks, const double *psi_table, int64_t table_len, double psi_k,
+                   double *out_te, void *workspace, size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ENTE_B200_H */

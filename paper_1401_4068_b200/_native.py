@@ -1,0 +1,146 @@
+"""ctypes binding of libente_b200.so (declared in include/ente_b200.h).
+
+There is no CPU fallback: importing the compute functions on a machine
+without the built library or without a CUDA device raises.  PyTorch is only
+the device-memory / stream plumbing: tensors are allocated with torch and
+their raw pointers handed to the C ABI together with the current stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+import torch
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libente_b200.so")
+
+CHUNK_OK, CHUNK_K_TOO_LARGE, CHUNK_NONFINITE, CHUNK_DEGENERATE = 0, 1, 2, 3
+
+
+class NativeError(RuntimeError):
+    """A C-ABI call returned an error code."""
+
+
+class ChunkDesc(ctypes.Structure):
+    _fields_ = [("row0", ctypes.c_int64), ("n", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def _declare(L):
+    vp, sz, i32, i64, dbl = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+    cp = ctypes.POINTER(ChunkDesc)
+    u32p = ctypes.POINTER(ctypes.c_uint32)
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    sig = {
+        "ente_version": ([], ctypes.c_char_p),
+        "ente_last_error": ([], ctypes.c_char_p),
+        "ente_search_workspace_size": ([cp, i32, i32, i32, i32], sz),
+        "ente_search": ([vp, i64, i32, cp, i32, u32p, i32, i32, vp, vp, vp, vp, sz, vp], i32),
+        "ente_radius_counts_workspace_size": ([i32], sz),
+        "ente_radius_counts": ([vp, i64, i32, cp, i32, u32p, i32, vp, vp, vp, vp, sz, vp], i32),
+        "ente_jitter_workspace_size": ([i32, i32], sz),
+        "ente_jitter": ([vp, i32, cp, i32, u64p, dbl, vp, vp, sz, vp], i32),
+        "ente_pack_te": ([vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32p, i32, vp, vp, vp], i32),
+        "ente_te_reduce_workspace_size": ([cp, i32], sz),
+        "ente_te_reduce": ([vp, i64, cp, i32, vp, i64, dbl, vp, vp, sz, vp], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+
+
+def lib():
+    """The loaded library (loaded once; raises if it was never built)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise ImportError(
+                        f"{LIB_PATH} is missing: build it with `python -m paper_1401_4068_b200.build` "
+                        "(there is no CPU fallback)")
+                L = ctypes.CDLL(LIB_PATH)
+                _declare(L)
+                _lib = L
+    return _lib
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1401_4068_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise NativeError(f"{what} failed ({rc}): {lib().ente_last_error().decode()}")
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def chunk_table(rows0, ns):
+    arr = (ChunkDesc * len(ns))()
+    for i, (r, n) in enumerate(zip(rows0, ns)):
+        arr[i].row0 = int(r)
+        arr[i].n = int(n)
+    return arr
+
+
+def ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+class _Workspace(threading.local):
+    buf = None
+
+
+_ws = _Workspace()
+
+
+def workspace(nbytes: int) -> torch.Tensor:
+    """A per-thread device scratch buffer of at least nbytes (grown on demand)."""
+    buf = _ws.buf
+    if buf is None or buf.numel() < nbytes or buf.device != device():
+        buf = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=device())
+        _ws.buf = buf
+    return buf
+
+
+def masks_array(masks):
+    arr = (ctypes.c_uint32 * max(1, len(masks)))()
+    for i, m in enumerate(masks):
+        arr[i] = int(m)
+    return arr
+
+
+def pcg_states(seeds, draws_per_seed):
+    """numpy PCG64 (state, inc) per seed as the uint64 quadruples of ente_jitter.
+
+    Mirrors np.random.default_rng(seed) as used by the reference jitter
+    (ksg.py:55): a Generator passed as seed is used as is and advanced by the
+    number of draws the reference would consume.
+    """
+    out = np.empty((len(seeds), 4), dtype=np.uint64)
+    mask = (1 << 64) - 1
+    for i, (seed, draws) in enumerate(zip(seeds, draws_per_seed)):
+        gen = np.random.default_rng(seed)
+        st = gen.bit_generator.state
+        if st.get("bit_generator") != "PCG64":
+            raise TypeError(f"jitter seeds must produce PCG64 generators, got {st.get('bit_generator')}")
+        s, inc = st["state"]["state"], st["state"]["inc"]
+        out[i] = (s >> 64, s & mask, inc >> 64, inc & mask)
+        if isinstance(seed, np.random.Generator):
+            gen.bit_generator.advance(int(draws))
+    return out

@@ -1,0 +1,237 @@
+// Tie-breaking jitter replica + degenerate / finiteness checks.
+//
+// Replaces ente.ksg._jittered_joint (/root/reference/pkg/src/ente/ksg.py:52-59)
+// and the checks of estimate_te_batch (ksg.py:80-81) / Chunk (engine.py:57-58).
+// numpy arithmetic is reproduced exactly:
+//   std   : column mean = sequential row-order sum / M; squared deviations
+//           summed sequentially / M; sqrt (numpy _var/_std over axis 0)
+//   U(-1,1): -1.0 + 2.0 * ((raw >> 11) * 2^-53), raw = PCG64 XSL-RR output
+//           of the state AFTER each LCG step, elements in C order
+//   update: x + (u * (amplitude * std)), two roundings, no FMA
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace ente {
+
+struct U128 {
+    uint64_t hi, lo;
+};
+
+__device__ __forceinline__ U128 mul128(U128 a, U128 b) {
+    U128 r;
+    r.lo = a.lo * b.lo;
+    r.hi = __umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo;
+    return r;
+}
+
+__device__ __forceinline__ U128 add128(U128 a, U128 b) {
+    U128 r;
+    r.lo = a.lo + b.lo;
+    r.hi = a.hi + b.hi + (r.lo < a.lo ? 1ull : 0ull);
+    return r;
+}
+
+// PCG_DEFAULT_MULTIPLIER_128 (numpy's PCG64)
+__device__ __constant__ U128 kPcgMult = {0x2360ED051FC65DA4ull, 0x4385DF649FCCF645ull};
+
+__device__ __forceinline__ uint64_t pcg_output(U128 s) {
+    const uint64_t x = s.hi ^ s.lo;
+    const unsigned rot = (unsigned)(s.hi >> 58);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+// state after `delta` LCG steps
+__device__ U128 pcg_advance(U128 state, U128 inc, uint64_t delta) {
+    U128 acc_mult = {0ull, 1ull}, acc_plus = {0ull, 0ull};
+    U128 cur_mult = kPcgMult, cur_plus = inc;
+    while (delta) {
+        if (delta & 1ull) {
+            acc_mult = mul128(acc_mult, cur_mult);
+            acc_plus = add128(mul128(acc_plus, cur_mult), cur_plus);
+        }
+        cur_plus = mul128(add128(cur_mult, U128{0ull, 1ull}), cur_plus);
+        cur_mult = mul128(cur_mult, cur_mult);
+        delta >>= 1;
+    }
+    return add128(mul128(acc_mult, state), acc_plus);
+}
+
+struct JitChunk {
+    int64_t row0;
+    int32_t n;
+    int32_t pad_;
+    U128 state, inc;
+};
+
+// one warp per chunk, one lane per column: numpy's sequential axis-0 sums
+__global__ void __launch_bounds__(32) jitter_std_kernel(const double *__restrict__ pts, int dim,
+                                                        const JitChunk *__restrict__ ch,
+                                                        double amplitude,
+                                                        double *__restrict__ half_width) {
+    const JitChunk c = ch[blockIdx.x];
+    const int col = threadIdx.x;
+    if (col >= dim) return;
+    const double *p = pts + c.row0 * dim + col;
+    double s = 0.0;
+#pragma unroll 8
+    for (int r = 0; r < c.n; ++r) s = __dadd_rn(s, p[(int64_t)r * dim]);
+    const double mean = __ddiv_rn(s, (double)c.n);
+    double v = 0.0;
+#pragma unroll 8
+    for (int r = 0; r < c.n; ++r) {
+        const double d = __dsub_rn(p[(int64_t)r * dim], mean);
+        v = __dadd_rn(v, __dmul_rn(d, d));
+    }
+    const double sd = __dsqrt_rn(__ddiv_rn(v, (double)c.n));
+    half_width[(int64_t)blockIdx.x * kMaxDim + col] = __dmul_rn(amplitude, sd);
+}
+
+constexpr int kJitPerThread = 64;
+
+__global__ void __launch_bounds__(256) jitter_apply_kernel(double *__restrict__ pts, int dim,
+                                                           const JitChunk *__restrict__ ch,
+                                                           const double *__restrict__ half_width) {
+    const JitChunk c = ch[blockIdx.y];
+    const int64_t total = (int64_t)c.n * dim;
+    const int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kJitPerThread;
+    if (e0 >= total) return;
+    const int64_t e1 = e0 + kJitPerThread < total ? e0 + kJitPerThread : total;
+    U128 s = pcg_advance(c.state, c.inc, (uint64_t)e0);
+    double *p = pts + c.row0 * dim;
+    const double *hw = half_width + (int64_t)blockIdx.y * kMaxDim;
+    int col = (int)(e0 % dim);
+    for (int64_t e = e0; e < e1; ++e) {
+        s = add128(mul128(s, kPcgMult), c.inc);
+        const uint64_t raw = pcg_output(s);
+        const double u01 = (double)(raw >> 11) * 0x1p-53;
+        const double u = __dadd_rn(-1.0, 2.0 * u01);
+        p[e] = __dadd_rn(p[e], __dmul_rn(u, hw[col]));
+        if (++col == dim) col = 0;
+    }
+}
+
+// status: non-finite beats degenerate (np.ptp of a NaN column is NaN != 0)
+__global__ void __launch_bounds__(256) check_kernel(const double *__restrict__ pts, int dim,
+                                                    const JitChunk *__restrict__ ch,
+                                                    int32_t *__restrict__ status) {
+    __shared__ double wmin[8][kMaxDim], wmax[8][kMaxDim];
+    __shared__ int bad;
+    const JitChunk c = ch[blockIdx.x];
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    const double *p = pts + c.row0 * dim;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int lbad = 0;
+    for (int q = 0; q < dim; ++q) {
+        double a = INFINITY, b = -INFINITY;
+        for (int r = threadIdx.x; r < c.n; r += blockDim.x) {
+            const double v = p[(int64_t)r * dim + q];
+            lbad |= !isfinite(v);
+            a = fmin(a, v);
+            b = fmax(b, v);
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+            a = fmin(a, __shfl_xor_sync(0xffffffffu, a, off));
+            b = fmax(b, __shfl_xor_sync(0xffffffffu, b, off));
+        }
+        if (lane == 0) {
+            wmin[warp][q] = a;
+            wmax[warp][q] = b;
+        }
+    }
+    if (lbad) bad = 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int st = ENTE_CHUNK_OK;
+        if (bad) {
+            st = ENTE_CHUNK_NONFINITE;
+        } else {
+            double ptp_max = 0.0;
+            for (int q = 0; q < dim; ++q) {
+                double a = wmin[0][q], b = wmax[0][q];
+                for (int w = 1; w < 8; ++w) {
+                    a = fmin(a, wmin[w][q]);
+                    b = fmax(b, wmax[w][q]);
+                }
+                ptp_max = fmax(ptp_max, b - a);
+            }
+            if (ptp_max == 0.0) st = ENTE_CHUNK_DEGENERATE;
+        }
+        if (status[blockIdx.x] == ENTE_CHUNK_OK) status[blockIdx.x] = st;
+    }
+}
+
+struct JitWs {
+    JitChunk *ch;
+    double *hw;
+};
+
+static JitWs jit_layout(Arena &a, int n_chunks) {
+    JitWs w;
+    w.ch = a.take<JitChunk>(n_chunks);
+    w.hw = a.take<double>((size_t)n_chunks * kMaxDim);
+    return w;
+}
+
+}  // namespace ente
+
+using namespace ente;
+
+extern "C" size_t ente_jitter_workspace_size(int n_chunks, int dim) {
+    (void)dim;
+    Arena a(nullptr, 0);
+    jit_layout(a, n_chunks);
+    return a.used + 256;
+}
+
+extern "C" int ente_jitter(double *pts64, int dim, const ente_chunk *chunks, int n_chunks,
+                           const uint64_t *pcg_state, double amplitude, int32_t *status,
+                           void *workspace, size_t ws_bytes, void *stream) {
+    if (n_chunks == 0) return ENTE_OK;
+    if (dim < 1 || dim > kMaxDim || n_chunks < 0 || !chunks || !pts64 || !status) {
+        set_error("ente_jitter: bad arguments (dim=%d, n_chunks=%d)", dim, n_chunks);
+        return ENTE_ERR_ARG;
+    }
+    if (amplitude > 0 && !pcg_state) {
+        set_error("ente_jitter: PCG64 states required when amplitude > 0");
+        return ENTE_ERR_ARG;
+    }
+    Arena a(workspace, ws_bytes);
+    JitWs w = jit_layout(a, n_chunks);
+    if (!a.ok() || !w.ch) {
+        set_error("ente_jitter: workspace of %zu bytes too small (need %zu)", ws_bytes, a.used);
+        return ENTE_ERR_WORKSPACE;
+    }
+    std::vector<JitChunk> h(n_chunks);
+    int max_n = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+        if (chunks[c].n < 1) {
+            set_error("ente_jitter: chunk %d has n=%d", c, chunks[c].n);
+            return ENTE_ERR_ARG;
+        }
+        h[c].row0 = chunks[c].row0;
+        h[c].n = chunks[c].n;
+        if (pcg_state) {
+            h[c].state = {pcg_state[4 * c + 0], pcg_state[4 * c + 1]};
+            h[c].inc = {pcg_state[4 * c + 2], pcg_state[4 * c + 3]};
+        }
+        max_n = max_n > chunks[c].n ? max_n : chunks[c].n;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ENTE_CUDA(cudaMemcpyAsync(w.ch, h.data(), sizeof(JitChunk) * n_chunks, cudaMemcpyHostToDevice, st));
+    if (amplitude > 0) {
+        jitter_std_kernel<<<n_chunks, 32, 0, st>>>(pts64, dim, w.ch, amplitude, w.hw);
+        ENTE_CUDA(cudaGetLastError());
+        const int64_t per_block = 256LL * kJitPerThread;
+        const int64_t gx = ((int64_t)max_n * dim + per_block - 1) / per_block;
+        dim3 grid((unsigned)gx, (unsigned)n_chunks);
+        jitter_apply_kernel<<<grid, 256, 0, st>>>(pts64, dim, w.ch, w.hw);
+        ENTE_CUDA(cudaGetLastError());
+    }
+    check_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.ch, status);
+    ENTE_CUDA(cudaGetLastError());
+    return ENTE_OK;
+}

@@ -1,0 +1,191 @@
+// KSG TE reduction: te = psi(k) + mean(sort(psi(a+1) - psi(b+1) - psi(c+1))).
+//
+// Replaces ente.ksg.te_from_counts (/root/reference/pkg/src/ente/ksg.py:39-49).
+// Bit-exact with the reference: the bracket is evaluated left to right from a
+// table of scipy digamma values, sorted ascending (stable LSD radix sort on
+// order-preserving 64-bit keys, one CTA per chunk), summed in numpy's
+// pairwise order (pairwise_sum: < 8 sequential, <= 128 eight accumulators,
+// else split at n/2 - (n/2) % 8) and divided by n.
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace ente {
+
+constexpr int kRedThreads = 256;
+constexpr int kRedWarps = kRedThreads / 32;
+
+__device__ __forceinline__ uint64_t f64_key(double v) {
+    const uint64_t b = (uint64_t)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ double key_f64(uint64_t k) {
+    const uint64_t b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+    return __longlong_as_double((long long)b);
+}
+
+__device__ double pairwise(const uint64_t *keys, int64_t n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, key_f64(keys[i]));
+        return res;
+    }
+    if (n <= 128) {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = key_f64(keys[j]);
+        int64_t i = 8;
+        for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], key_f64(keys[i + j]));
+        }
+        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; ++i) res = __dadd_rn(res, key_f64(keys[i]));
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return __dadd_rn(pairwise(keys, n2), pairwise(keys + n2, n - n2));
+}
+
+struct RedChunk {
+    int64_t row0;
+    int32_t n;
+    int32_t pad_;
+};
+
+__global__ void __launch_bounds__(kRedThreads) te_reduce_kernel(
+    const int32_t *__restrict__ counts, int64_t total_rows, const RedChunk *__restrict__ chunks,
+    const double *__restrict__ psi, int64_t table_len, double psi_k, uint64_t *__restrict__ ka,
+    uint64_t *__restrict__ kb, double *__restrict__ out_te) {
+    __shared__ int hist[256];
+    __shared__ int wcnt[kRedWarps][256];
+    __shared__ int bad;
+    const RedChunk ch = chunks[blockIdx.x];
+    const int n = ch.n;
+    uint64_t *src = ka + ch.row0;
+    uint64_t *dst = kb + ch.row0;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += kRedThreads) {
+        const int64_t row = ch.row0 + i;
+        const int a = counts[row], b = counts[total_rows + row], c = counts[2 * total_rows + row];
+        double v = 0.0;
+        if (a < 0 || b < 0 || c < 0 || a >= table_len || b >= table_len || c >= table_len) bad = 1;
+        else v = __dsub_rn(__dsub_rn(psi[a], psi[b]), psi[c]);
+        src[i] = f64_key(v);
+    }
+    __syncthreads();
+    if (bad) {
+        if (threadIdx.x == 0) out_te[blockIdx.x] = __longlong_as_double(0x7FF8000000000000ll);
+        return;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    for (int shift = 0; shift < 64; shift += 8) {
+        hist[threadIdx.x] = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += kRedThreads) atomicAdd(&hist[(src[i] >> shift) & 255], 1);
+        __syncthreads();
+        bool single = false;
+        for (int d = 0; d < 256; ++d) single |= hist[d] == n;
+        __syncthreads();
+        if (single) continue;  // every key shares this digit: the pass is the identity
+        if (threadIdx.x == 0) {
+            int run = 0;
+            for (int d = 0; d < 256; ++d) {
+                const int h = hist[d];
+                hist[d] = run;
+                run += h;
+            }
+        }
+        __syncthreads();
+        // stable scatter, one 256-key tile at a time in input order
+        for (int base = 0; base < n; base += kRedThreads) {
+            const int i = base + threadIdx.x;
+            const bool valid = i < n;
+            const uint64_t key = valid ? src[i] : 0ull;
+            const int dig = valid ? (int)((key >> shift) & 255) : 256 + warp;
+#pragma unroll
+            for (int w = 0; w < kRedWarps; ++w) wcnt[w][threadIdx.x] = 0;
+            __syncthreads();
+            const unsigned peers = __match_any_sync(0xffffffffu, dig);
+            const int rank = __popc(peers & lt_mask);
+            if (valid && rank == 0) wcnt[warp][dig] = __popc(peers);
+            __syncthreads();
+            if (valid) {
+                int pre = 0;
+                for (int w = 0; w < warp; ++w) pre += wcnt[w][dig];
+                dst[hist[dig] + pre + rank] = key;
+            }
+            __syncthreads();
+            int add = 0;
+#pragma unroll
+            for (int w = 0; w < kRedWarps; ++w) add += wcnt[w][threadIdx.x];
+            hist[threadIdx.x] += add;
+            __syncthreads();
+        }
+        uint64_t *t = src;
+        src = dst;
+        dst = t;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double sum = pairwise(src, n);
+        out_te[blockIdx.x] = __dadd_rn(psi_k, __ddiv_rn(sum, (double)n));
+    }
+}
+
+}  // namespace ente
+
+using namespace ente;
+
+extern "C" size_t ente_te_reduce_workspace_size(const ente_chunk *chunks, int n_chunks) {
+    int64_t rows = 0;
+    for (int c = 0; c < n_chunks; ++c) rows = rows > chunks[c].row0 + chunks[c].n ? rows : chunks[c].row0 + chunks[c].n;
+    Arena a(nullptr, 0);
+    a.take<RedChunk>(n_chunks);
+    a.take<uint64_t>(rows);
+    a.take<uint64_t>(rows);
+    return a.used + 256;
+}
+
+extern "C" int ente_te_reduce(const int32_t *counts, int64_t total_rows, const ente_chunk *chunks,
+                              int n_chunks, const double *psi_table, int64_t table_len,
+                              double psi_k, double *out_te, void *workspace, size_t ws_bytes,
+                              void *stream) {
+    if (n_chunks == 0) return ENTE_OK;
+    if (n_chunks < 0 || !chunks || !counts || !psi_table || !out_te || table_len < 1) {
+        set_error("ente_te_reduce: bad arguments");
+        return ENTE_ERR_ARG;
+    }
+    int64_t rows = 0;
+    std::vector<RedChunk> h(n_chunks);
+    for (int c = 0; c < n_chunks; ++c) {
+        if (chunks[c].n < 1 || chunks[c].row0 < 0 || chunks[c].row0 + chunks[c].n > total_rows) {
+            set_error("ente_te_reduce: chunk %d outside the count rows", c);
+            return ENTE_ERR_ARG;
+        }
+        h[c].row0 = chunks[c].row0;
+        h[c].n = chunks[c].n;
+        rows = rows > chunks[c].row0 + chunks[c].n ? rows : chunks[c].row0 + chunks[c].n;
+    }
+    Arena a(workspace, ws_bytes);
+    RedChunk *dch = a.take<RedChunk>(n_chunks);
+    uint64_t *ka = a.take<uint64_t>(rows);
+    uint64_t *kb = a.take<uint64_t>(rows);
+    if (!a.ok() || !dch) {
+        set_error("ente_te_reduce: workspace of %zu bytes too small (need %zu)", ws_bytes, a.used);
+        return ENTE_ERR_WORKSPACE;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ENTE_CUDA(cudaMemcpyAsync(dch, h.data(), sizeof(RedChunk) * n_chunks, cudaMemcpyHostToDevice, st));
+    te_reduce_kernel<<<n_chunks, kRedThreads, 0, st>>>(counts, total_rows, dch, psi_table, table_len,
+                                                      psi_k, ka, kb, out_te);
+    ENTE_CUDA(cudaGetLastError());
+    return ENTE_OK;
+}

@@ -1,0 +1,200 @@
+"""Batched exact max-norm kNN distances and strict radius counts on the GPU.
+
+Drop-in for the reference neighbour engine
+(/root/reference/pkg/src/ente/engine.py): same names, argument meaning,
+outputs (float64 kth_distance, int64 counts, input order) and per-chunk
+error slots.  All arithmetic runs in the sm_100a kernels of
+libente_b200.so (ente_search / ente_radius_counts); results are
+bit-identical to the reference's fp64 sweep.
+
+  Chunk              engine.py:46-59     NeighborCounts   engine.py:62-67
+  knn_kth_distances  engine.py:170-176   radius_counts    engine.py:179-188
+  batch_search       engine.py:203-216   set_workers / max_workers 31-43
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .exceptions import KTooLarge, ShapeMismatch
+
+MAX_DIM = 32   # column bitmasks are uint32 in the C ABI
+MAX_K = 64     # exact warp top-k merge keeps <= 64 slots per lane
+MAX_MARG = 8
+
+_workers = [os.cpu_count() or 1]
+
+
+def max_workers() -> int:
+    """Host threads available for host-side preparation (seeding, permutations)."""
+    return os.cpu_count() or 1
+
+
+def set_workers(n: int) -> int:
+    """Set the host worker count (never changes results); returns the count in effect."""
+    _workers[0] = max(1, min(int(n), max_workers()))
+    return _workers[0]
+
+
+@dataclass(frozen=True)
+class Chunk:
+    """One search problem: an [n >= 2, dim >= 1] finite point matrix (fp64 copy)."""
+
+    points: np.ndarray
+    chunk_id: int = 0
+
+    def __post_init__(self):
+        pts = np.ascontiguousarray(np.asarray(self.points, dtype=np.float64))
+        if pts.ndim != 2 or pts.shape[0] < 2 or pts.shape[1] < 1:
+            raise ShapeMismatch(f"chunk needs an [n>=2 x dim>=1] matrix, got {pts.shape}")
+        if not np.isfinite(pts).all():
+            raise ShapeMismatch("chunk contains non-finite values")
+        object.__setattr__(self, "points", pts)
+
+
+@dataclass(frozen=True)
+class NeighborCounts:
+    """kth_distance (float64 [n]) and one int64 [n] count array per marginal."""
+
+    kth_distance: np.ndarray
+    radius_counts: tuple
+
+
+def column_mask(cols, dim: int) -> int:
+    cols = np.asarray(cols, dtype=np.intp).ravel()
+    if cols.size < 1 or cols.min() < 0 or cols.max() >= dim:
+        raise ShapeMismatch(f"marginal columns {cols} out of range")
+    mask = 0
+    for c in cols.tolist():
+        mask |= 1 << c
+    return mask
+
+
+# ---------------------------------------------------------------------------
+# device-level entry points (tensors in, tensors out; used by ksg / bench)
+# ---------------------------------------------------------------------------
+def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int):
+    """ente_search on a device-resident [rows, dim] fp64 matrix.
+
+    Returns (eps [rows] f64, counts [n_marg, rows] int32, status [n_chunks] int32),
+    all on the device, stream-ordered on the current stream.
+    """
+    if pts64.dtype != torch.float64 or not pts64.is_cuda or not pts64.is_contiguous():
+        raise TypeError("pts64 must be a contiguous CUDA float64 tensor")
+    rows, dim = pts64.shape
+    L = nat.lib()
+    table = nat.chunk_table(rows0, ns)
+    marr = nat.masks_array(masks)
+    eps = torch.empty(rows, dtype=torch.float64, device=pts64.device)
+    counts = torch.empty((max(1, len(masks)), rows), dtype=torch.int32, device=pts64.device)
+    status = torch.empty(max(1, len(ns)), dtype=torch.int32, device=pts64.device)
+    need = L.ente_search_workspace_size(table, len(ns), dim, len(masks), int(k))
+    ws = nat.workspace(need)
+    nat.check(L.ente_search(nat.ptr(pts64), rows, dim, table, len(ns), marr, len(masks), int(k),
+                            nat.ptr(eps), nat.ptr(counts), nat.ptr(status), nat.ptr(ws), ws.numel(),
+                            nat.stream_handle()), "ente_search")
+    return eps, counts[:len(masks)], status[:len(ns)]
+
+
+def _upload(points_list):
+    host = np.ascontiguousarray(np.concatenate(points_list, axis=0), dtype=np.float64)
+    t = torch.from_numpy(host)
+    if torch.cuda.is_available():
+        t = t.pin_memory()
+    return t.to(nat.device(), non_blocking=True)
+
+
+def _run_group(points_list, dim, masks, k):
+    ns = [p.shape[0] for p in points_list]
+    rows0 = np.concatenate([[0], np.cumsum(ns)[:-1]]).astype(np.int64)
+    dev = _upload(points_list)
+    eps, counts, status = search_device(dev, rows0, ns, masks, k)
+    eps_h = eps.cpu().numpy()
+    cnt_h = counts.cpu().numpy().astype(np.int64)
+    st_h = status.cpu().numpy()
+    out = []
+    for i, (r0, n) in enumerate(zip(rows0, ns)):
+        if st_h[i] == nat.CHUNK_NONFINITE:
+            out.append(ShapeMismatch("chunk contains non-finite values"))
+        elif st_h[i] == nat.CHUNK_K_TOO_LARGE:
+            out.append(KTooLarge(f"k={k} not in [1, n-1] for n={n}"))
+        else:
+            sl = slice(r0, r0 + n)
+            out.append(NeighborCounts(eps_h[sl].copy(), tuple(cnt_h[m, sl].copy()
+                                                              for m in range(len(masks)))))
+    return out
+
+
+def batch_search(items: Sequence, k: int):
+    """kNN + marginal radius counts for many chunks; one slot per chunk, in order.
+
+    Each slot is a NeighborCounts or the exception raised for that chunk
+    (KTooLarge before ShapeMismatch, as engine.py:191-200 checks them).
+    Chunks sharing (dim, marginal layout) go to the GPU in one launch sequence.
+    """
+    results = [None] * len(items)
+    groups = {}
+    for slot, (chunk, marginals) in enumerate(items):
+        pts = np.ascontiguousarray(np.asarray(chunk.points, dtype=np.float64))
+        n, dim = pts.shape
+        if k < 1 or k > n - 1:
+            results[slot] = KTooLarge(f"k={k} not in [1, n-1] for n={n}")
+            continue
+        try:
+            masks = tuple(column_mask(cols, dim) for cols in marginals)
+        except ShapeMismatch as exc:
+            results[slot] = exc
+            continue
+        if dim > MAX_DIM or k > MAX_K or len(masks) > MAX_MARG:
+            results[slot] = NotImplementedError(
+                f"dim={dim} (<= {MAX_DIM}), k={k} (<= {MAX_K}), marginals={len(masks)} "
+                f"(<= {MAX_MARG}) exceed the compiled engine limits")
+            continue
+        groups.setdefault((dim, masks), []).append((slot, pts))
+    for (dim, masks), members in groups.items():
+        outs = _run_group([p for _, p in members], dim, list(masks), k)
+        for (slot, _), res in zip(members, outs):
+            results[slot] = res
+    return results
+
+
+def knn_kth_distances(chunk: Chunk, k: int) -> np.ndarray:
+    """Distance from each point to its k-th nearest neighbour (self excluded)."""
+    n = chunk.points.shape[0]
+    if k < 1 or k > n - 1:
+        raise KTooLarge(f"k={k} not in [1, n-1] for n={n}")
+    (res,) = batch_search([(chunk, [])], k)
+    if isinstance(res, Exception):
+        raise res
+    return res.kth_distance
+
+
+def radius_counts(chunk: Chunk, radii) -> np.ndarray:
+    """#{j != i : maxnorm(p_i, p_j) < radii[i]} over all columns of the chunk."""
+    radii = np.ascontiguousarray(np.asarray(radii, dtype=np.float64))
+    pts = chunk.points
+    n, dim = pts.shape
+    if radii.shape != (n,):
+        raise ShapeMismatch(f"radii shape {radii.shape} does not match n={n}")
+    if (radii < 0).any():
+        raise ShapeMismatch("radii must be nonnegative")
+    if dim > MAX_DIM:
+        raise NotImplementedError(f"dim={dim} exceeds {MAX_DIM}")
+    L = nat.lib()
+    dev = _upload([pts])
+    r = torch.from_numpy(radii).to(dev.device)
+    counts = torch.empty((1, n), dtype=torch.int32, device=dev.device)
+    status = torch.empty(1, dtype=torch.int32, device=dev.device)
+    table = nat.chunk_table([0], [n])
+    marr = nat.masks_array([(1 << dim) - 1])
+    ws = nat.workspace(L.ente_radius_counts_workspace_size(1))
+    nat.check(L.ente_radius_counts(nat.ptr(dev), n, dim, table, 1, marr, 1, nat.ptr(r),
+                                   nat.ptr(counts), nat.ptr(status), nat.ptr(ws), ws.numel(),
+                                   nat.stream_handle()), "ente_radius_counts")
+    return counts[0].cpu().numpy().astype(np.int64)

@@ -1,0 +1,274 @@
+"""Surrogate testing and delay scanning; every TE of a pair in one device batch.
+
+Drop-in for /root/reference/pkg/src/ente/inference.py: SurrogateSpec 27-38,
+draw_permutation 41-49, shuffle_target 52-59, permutation_pvalue 62-74,
+correct_multiple 77-98, _surrogate_seed 101-102, _permuted_bundle 105-117,
+analyze_pair 120-193, scan_delays 196-200, analyze_pairs 203-216.
+
+analyze_pair differs from the reference only in HOW it computes: instead of
+one estimate_te_batch call per u (inference.py:147,173) it packs every
+(u, surrogate) chunk on the device from the two ensembles (ente_pack_te),
+jitters, searches and reduces them in one pipeline, then runs the same host
+statistics.  Permutations and jitter states are derived exactly as the
+reference derives them (numpy SeedSequence / Generator) and cached per
+(seed, index), so repeated windows and pairs reuse them.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .data import AnalysisConfig, EnsembleSeries, TEResult, validate_ensemble
+from .embedding import EmbeddingSpec, PointSetBundle, check_assembly
+from .exceptions import EnteError, InvalidPermutation, KTooLarge, UnknownMethod
+from .ksg import _raise_status, te_chunks_device
+
+# rows per device wave (fp64 joint + fp32 copy + counts + events ~ 150 B/row)
+MAX_ROWS_PER_WAVE = 1 << 28
+
+
+@dataclass(frozen=True)
+class SurrogateSpec:
+    """A repetition permutation phi (0-based) and the seed it came from."""
+
+    permutation: np.ndarray
+    seed: object = None
+
+    def __post_init__(self):
+        perm = np.asarray(self.permutation, dtype=np.int64)
+        object.__setattr__(self, "permutation", perm)
+        if perm.ndim != 1 or not np.array_equal(np.sort(perm), np.arange(perm.size)):
+            raise InvalidPermutation("not a bijection on {0..R-1}")
+
+
+def draw_permutation(n_repetitions: int, seed, strict: bool = True) -> SurrogateSpec:
+    """numpy permutation of range(R); with strict, redrawn until phi(r) != r for all r."""
+    if strict and n_repetitions < 2:
+        raise InvalidPermutation("strict permutation needs R >= 2")
+    gen = np.random.default_rng(seed)
+    ident = np.arange(n_repetitions)
+    perm = gen.permutation(n_repetitions)
+    while strict and (perm == ident).any():
+        perm = gen.permutation(n_repetitions)
+    return SurrogateSpec(perm, seed)
+
+
+def shuffle_target(target: EnsembleSeries, spec: SurrogateSpec) -> EnsembleSeries:
+    """Target with repetition r replaced by repetition phi(r) (input untouched)."""
+    if spec.permutation.size != target.n_repetitions:
+        raise InvalidPermutation(
+            f"permutation length {spec.permutation.size} != R={target.n_repetitions}")
+    return EnsembleSeries(target.channel_name, target.values[spec.permutation],
+                          target.sample_rate)
+
+
+def permutation_pvalue(te_original: float, te_surrogates, conservative: bool = False) -> float:
+    surr = np.asarray(te_surrogates, dtype=np.float64)
+    if surr.size < 1:
+        raise ValueError("need at least one surrogate value")
+    hits = int(np.count_nonzero(surr >= te_original))
+    return (hits + 1) / (surr.size + 1) if conservative else hits / surr.size
+
+
+def correct_multiple(pvalues, alpha: float, method: str = "bonferroni"):
+    """Family-wise decisions: none (p < a), bonferroni (p < a/m), fdr (BH step-up)."""
+    p = np.asarray(pvalues, dtype=np.float64)
+    m = p.size
+    if method == "none":
+        return (p < alpha).tolist()
+    if method == "bonferroni":
+        return (p < alpha / m).tolist()
+    if method == "fdr":
+        ranked = np.sort(p, kind="stable")
+        ok = np.flatnonzero(ranked <= alpha * np.arange(1, m + 1) / m)
+        if ok.size == 0:
+            return [False] * m
+        return (p <= ranked[ok[-1]]).tolist()
+    raise UnknownMethod(f"unknown correction method {method!r}")
+
+
+def _surrogate_seed(master_seed, index: int):
+    return np.random.SeedSequence((master_seed, index))
+
+
+def _permuted_bundle(bundle: PointSetBundle, permutation: np.ndarray,
+                     window_width: int) -> PointSetBundle:
+    """Host form of the surrogate joint: y columns take block rows perm[r]*w + t."""
+    src_rows = (np.asarray(permutation)[:, None] * window_width
+                + np.arange(window_width)[None, :]).reshape(-1)
+    joint = bundle.joint.copy()
+    ny = 1 + bundle.d_y
+    joint[:, :ny] = bundle.joint[src_rows, :ny]
+    return PointSetBundle(joint, bundle.d_y, bundle.d_x, bundle.row_origin)
+
+
+# ---------------------------------------------------------------------------
+# host prep caches (pure functions of their keys)
+# ---------------------------------------------------------------------------
+_PERMS: dict = {}
+_STATES: dict = {}
+_MASK64 = (1 << 64) - 1
+
+
+def cached_permutation(master_seed, idx: int, reps: int, strict: bool) -> np.ndarray:
+    key = (master_seed, idx, reps, strict)
+    perm = _PERMS.get(key)
+    if perm is None:
+        perm = draw_permutation(reps, _surrogate_seed(master_seed, idx), strict).permutation
+        if len(_PERMS) < 1 << 20:
+            _PERMS[key] = perm
+    return perm
+
+
+def jitter_state(seed_tuple) -> tuple:
+    """PCG64 (state, inc) of default_rng(SeedSequence(seed_tuple)) as 4 uint64."""
+    st = _STATES.get(seed_tuple)
+    if st is None:
+        s = np.random.PCG64(np.random.SeedSequence(seed_tuple)).state["state"]
+        st = (s["state"] >> 64, s["state"] & _MASK64, s["inc"] >> 64, s["inc"] & _MASK64)
+        if len(_STATES) < 1 << 22:
+            _STATES[seed_tuple] = st
+    return st
+
+
+class PairPipeline:
+    """Device pipeline for the chunks of one (source, target) pair.
+
+    run(items) takes (u, perm_index) items (perm_index -1 = original data)
+    and returns their TE values in order; errors are raised for the first
+    failing item, as the reference's per-u estimate_te_batch calls would.
+    """
+
+    def __init__(self, source, target, spec_x, spec_y, config: AnalysisConfig):
+        self.cfg = config
+        self.sx, self.sy = spec_x, spec_y
+        self.reps, self.n_samples = target.values.shape
+        self.t_lo, self.t_hi = config.window
+        self.w = self.t_hi - self.t_lo + 1
+        self.m = self.reps * self.w
+        self.dim = 1 + spec_y.dim + spec_x.dim
+        dev = nat.device()
+        self.x = torch.from_numpy(np.array(source.values, dtype=np.float64)).to(dev)
+        self.y = torch.from_numpy(np.array(target.values, dtype=np.float64)).to(dev)
+        self.perm_dev = None
+        self.perm_count = 0
+
+    def set_perms(self, perms):
+        arr = np.ascontiguousarray(np.stack(perms).astype(np.int32))
+        self.perm_dev = torch.from_numpy(arr).to(nat.device())
+        self.perm_count = len(perms)
+
+    def seed_tuple(self, u, perm_index):
+        return (self.cfg.seed, u, 0 if perm_index < 0 else perm_index + 1)
+
+    def run(self, items) -> np.ndarray:
+        if not items:
+            return np.empty(0)
+        if self.m <= self.cfg.k:
+            raise KTooLarge(f"need more than k={self.cfg.k} pooled points, got {self.m}")
+        per_wave = max(1, MAX_ROWS_PER_WAVE // self.m)
+        out = []
+        for s in range(0, len(items), per_wave):
+            out.append(self._wave(items[s:s + per_wave]))
+        return np.concatenate(out)
+
+    def _wave(self, items) -> np.ndarray:
+        L = nat.lib()
+        n = len(items)
+        it = np.ascontiguousarray(np.array(items, dtype=np.int32).reshape(n, 2))
+        pts = torch.empty((n * self.m, self.dim), dtype=torch.float64, device=self.x.device)
+        perms_ptr = nat.ptr(self.perm_dev) if self.perm_dev is not None else None
+        nat.check(L.ente_pack_te(nat.ptr(self.x), nat.ptr(self.y), self.reps, self.n_samples,
+                                 self.sx.dim, self.sx.delay, self.sy.dim, self.sy.delay,
+                                 self.t_lo, self.t_hi,
+                                 it.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_int32)), n,
+                                 perms_ptr, nat.ptr(pts), nat.stream_handle()), "ente_pack_te")
+        rows0 = np.arange(n, dtype=np.int64) * self.m
+        ns = [self.m] * n
+        states = np.array([jitter_state(self.seed_tuple(u, p)) for u, p in items],
+                          dtype=np.uint64)
+        te, st = te_chunks_device(pts, rows0, ns, self.sy.dim, self.sx.dim, self.cfg.k,
+                                  self.cfg.jitter_amplitude, states)
+        if te is None:
+            _raise_status(int(st[np.flatnonzero(st)[0]]))
+        return te.cpu().numpy()
+
+
+def analyze_pair(source: EnsembleSeries, target: EnsembleSeries,
+                 spec_x: EmbeddingSpec, spec_y: EmbeddingSpec,
+                 config: AnalysisConfig) -> TEResult:
+    """Delay scan + surrogate test for one directed pair in one window (TE in nats)."""
+    validate_ensemble(source)
+    validate_ensemble(target)
+    selected = config.scan_statistic == "selected"
+    grid = None if selected else (config.test_grid or config.u_candidates)
+    us = list(config.u_candidates)
+    assembly_error = None
+    for i, u in enumerate(us):
+        try:
+            check_assembly(source, target, spec_x, spec_y, u, config.window)
+        except EnteError as exc:
+            assembly_error = exc
+            us = us[:i]
+            break
+    pipe = PairPipeline(source, target, spec_x, spec_y, config)
+    reps = target.n_repetitions
+    s = config.n_surrogates
+    can_draw = reps >= 2 or not config.strict_permutation
+    originals = [(u, -1) for u in us]
+
+    if not selected and assembly_error is None and can_draw:
+        perms = [cached_permutation(config.seed, i, reps, config.strict_permutation)
+                 for i in range(s)]
+        pipe.set_perms(perms)
+        surr_items = [(u, i) for u in grid for i in range(s)]
+        te_all = pipe.run(originals + surr_items)
+        te_orig = te_all[:len(us)]
+        te_surr = te_all[len(us):].reshape(len(grid), s)
+    else:
+        te_orig = pipe.run(originals)
+        if assembly_error is not None:
+            raise assembly_error
+        te_surr = None
+    curve = [(u, float(t)) for u, t in zip(us, te_orig)]
+    u_best, te_best = max(curve, key=lambda ut: (ut[1], -ut[0]))
+    if grid is None:
+        grid = (u_best,)
+        stat_orig = te_best
+    else:
+        stat_orig = max(t for u, t in curve if u in grid)
+    if te_surr is None:
+        perms = [cached_permutation(config.seed, i, reps, config.strict_permutation)
+                 for i in range(s)]
+        pipe.set_perms(perms)
+        te_surr = pipe.run([(u, i) for u in grid for i in range(s)]).reshape(len(grid), s)
+    surrogates = np.full(s, -np.inf)
+    for row in te_surr:
+        np.maximum(surrogates, row, out=surrogates)
+    p = permutation_pvalue(stat_orig, surrogates, config.conservative_pvalue)
+    sig = p < config.alpha
+    return TEResult(source=source.channel_name, target=target.channel_name,
+                    window=config.window, u_selected=u_best, te_value=te_best,
+                    surrogate_values=surrogates, p_value=p, significant=sig,
+                    significant_corrected=sig,
+                    te_minus_median_surrogate=te_best - float(np.median(surrogates)),
+                    te_curve=curve)
+
+
+def scan_delays(source, target, spec_x, spec_y, config) -> TEResult:
+    """Alias of analyze_pair (which always scans)."""
+    return analyze_pair(source, target, spec_x, spec_y, config)
+
+
+def analyze_pairs(series_by_name: dict, pairs, specs_by_name: dict, config: AnalysisConfig):
+    """analyze_pair per directed pair + the configured family-wise correction."""
+    results = [analyze_pair(series_by_name[a], series_by_name[b], specs_by_name[a],
+                            specs_by_name[b], config) for a, b in pairs]
+    decisions = correct_multiple([r.p_value for r in results], config.alpha, config.correction)
+    for r, d in zip(results, decisions):
+        r.significant_corrected = bool(d and r.significant)
+    return results

@@ -1,0 +1,156 @@
+"""GPU parity of the neighbour engine: bit-exact vs the reference goldens and the oracle.
+
+Reference tests mirrored: pkg/tests/test_engine.py (hand examples, random and
+tied chunks vs O(n^2), validation, error slots, worker invariance) and the
+engine-oracle acceptance criterion (test_acceptance.py:198-247).
+"""
+
+import numpy as np
+import pytest
+
+import cases
+import oracle
+from paper_1401_4068_b200.engine import (Chunk, batch_search, knn_kth_distances,
+                                         radius_counts)
+from paper_1401_4068_b200.exceptions import KTooLarge, ShapeMismatch
+
+pytestmark = pytest.mark.gpu
+
+GROUPS = [("hand", cases.hand_cases), ("random", cases.engine_random_chunks),
+          ("tie", cases.engine_tie_chunk), ("c6", cases.criterion6_chunks),
+          ("telayout", cases.te_layout_chunks)]
+
+
+def run_group(cl):
+    eps, cnt = [], []
+    by_k = {}
+    for i, (p, m, k) in enumerate(cl):
+        by_k.setdefault(k, []).append(i)
+    res = [None] * len(cl)
+    for k, idx in by_k.items():
+        out = batch_search([(Chunk(cl[i][0]), cl[i][1]) for i in idx], k)
+        for i, r in zip(idx, out):
+            res[i] = r
+    for r in res:
+        assert not isinstance(r, Exception), r
+        eps.append(r.kth_distance)
+        cnt += list(r.radius_counts)
+    return np.concatenate(eps), np.concatenate(cnt)
+
+
+@pytest.mark.parametrize("name,gen", GROUPS)
+def test_engine_bit_exact_vs_reference_goldens(golden, name, gen):
+    g = golden("engine.npz")
+    cl = gen()
+    assert cases.sha(*[p for p, _, _ in cl]) == str(g[f"{name}_sha"])
+    eps, cnt = run_group(cl)
+    assert eps.dtype == np.float64
+    assert np.array_equal(eps, g[f"{name}_eps"])
+    assert np.array_equal(cnt, g[f"{name}_counts"])
+
+
+def test_hand_examples():
+    eps = knn_kth_distances(Chunk(np.array([[0.0], [0.3], [1.0], [2.0]])), 2)
+    assert np.allclose(eps, [1.0, 0.7, 1.0, 1.7])
+    pts = Chunk(np.array([[0.0], [1.0], [2.0]]))
+    assert radius_counts(pts, np.array([1.0, 1.0, 1.0])).tolist() == [0, 0, 0]
+    assert radius_counts(pts, np.array([1.5, 1.5, 1.5])).tolist() == [1, 2, 1]
+
+
+def _te_case(rng, n, d_y, d_x, kind):
+    d = 1 + d_y + d_x
+    pts = rng.standard_normal((n, d))
+    if kind == "round":
+        pts = np.round(pts, 1)
+    elif kind == "offset":
+        pts = pts * 1e-4 + 5e3
+    elif kind == "dup":
+        pts[n // 2:] = pts[: n - n // 2]
+    elif kind == "lowdim":
+        t = rng.standard_normal((n, 1))
+        pts = np.concatenate([t + 1e-3 * rng.standard_normal((n, 1)) for _ in range(d)], axis=1)
+    return pts, cases.te_margs(d_y, d_x)
+
+
+@pytest.mark.parametrize("kind", ["normal", "round", "offset", "dup", "lowdim"])
+def test_fast_path_vs_oracle_multi_chunk(kind):
+    rng = np.random.default_rng(hash(kind) % 2 ** 32)
+    for d_y, d_x in [(1, 1), (2, 2), (3, 3), (2, 3), (8, 8)]:
+        items, ref = [], []
+        for n in (5, 129, 700, 1500):
+            pts, margs = _te_case(rng, n, d_y, d_x, kind)
+            items.append((Chunk(pts), margs))
+            ref.append(oracle.search(pts, margs, 4))
+        for (e, c), r in zip(ref, batch_search(items, 4)):
+            assert np.array_equal(r.kth_distance, e)
+            for a, b in zip(r.radius_counts, c):
+                assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 8, 15, 16, 20])
+def test_all_k_vs_oracle(k):
+    rng = np.random.default_rng(k)
+    pts = np.round(rng.standard_normal((900, 5)), 2)
+    margs = cases.te_margs(2, 2) + [[0], [4, 1]]
+    (r,) = batch_search([(Chunk(pts), margs)], k)
+    e, c = oracle.search(pts, margs, k)
+    assert np.array_equal(r.kth_distance, e)
+    for a, b in zip(r.radius_counts, c):
+        assert np.array_equal(a, b)
+
+
+def test_bench_layout_paper_geometry_sample():
+    # paper geometry columns: joint 17, marginal = first 8 (bench.py:56)
+    rng = np.random.default_rng(0)
+    pts = rng.standard_normal((3000, 17))
+    (r,) = batch_search([(Chunk(pts), [list(range(8))])], 4)
+    e, (c,) = oracle.search(pts, [list(range(8))], 4)
+    assert np.array_equal(r.kth_distance, e) and np.array_equal(r.radius_counts[0], c)
+
+
+def test_errors_are_isolated_per_slot():
+    rng = np.random.default_rng(0)
+    good = Chunk(rng.standard_normal((20, 3)))
+    res = batch_search([(good, [[0], [0, 1]]), (good, [[0, 7]]), (good, [[2]]),
+                        (Chunk(rng.standard_normal((3, 3))), [[0]])], k=3)
+    assert not isinstance(res[0], Exception)
+    assert isinstance(res[1], ShapeMismatch)
+    assert not isinstance(res[2], Exception)
+    assert isinstance(res[3], KTooLarge)
+    assert np.array_equal(res[0].kth_distance, res[2].kth_distance)
+    with pytest.raises(KTooLarge):
+        knn_kth_distances(Chunk(np.arange(10.0).reshape(5, 2)), 5)
+    with pytest.raises(ShapeMismatch):
+        radius_counts(Chunk(np.arange(6.0).reshape(3, 2)), np.array([1.0, -1.0, 2.0]))
+
+
+def test_strict_count_bound_and_monotone_k():
+    rng = np.random.default_rng(4)
+    pts = rng.standard_normal((400, 3))
+    ch = Chunk(pts)
+    prev = None
+    for k in (1, 2, 3, 4):
+        (r,) = batch_search([(ch, [[0, 1, 2]])], k)
+        assert np.all(r.radius_counts[0] <= k - 1)
+        if prev is not None:
+            assert np.all(r.kth_distance >= prev)
+        prev = r.kth_distance
+
+
+def test_translation_and_scale():
+    rng = np.random.default_rng(9)
+    pts = rng.standard_normal((600, 5))
+    e = knn_kth_distances(Chunk(pts), 4)
+    assert np.allclose(knn_kth_distances(Chunk(pts + 7.25), 4), e, rtol=0, atol=1e-9)
+    assert np.allclose(knn_kth_distances(Chunk(pts * 2.0), 4), 2.0 * e, rtol=1e-12, atol=0)
+
+
+def test_batch_equals_singles():
+    rng = np.random.default_rng(5)
+    chunks = [Chunk(rng.standard_normal((n, 7))) for n in (300, 1000, 2048)]
+    margs = cases.te_margs(3, 3)
+    batch = batch_search([(c, margs) for c in chunks], 4)
+    for c, b in zip(chunks, batch):
+        (s,) = batch_search([(c, margs)], 4)
+        assert np.array_equal(s.kth_distance, b.kth_distance)
+        assert all(np.array_equal(x, y) for x, y in zip(s.radius_counts, b.radius_counts))
