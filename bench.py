@@ -1,0 +1,330 @@
+"""Benchmark of the ensemble-TE hot path (BASELINE.json metric, config C2 by default).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C2|C1|C4|C5] [--surrogates S]
+
+One STEP = one full analyze_pair workload of the config: every (u, surrogate)
+chunk (C2: 10 originals + 10 x 200 surrogates = 2010 chunks of 30000 points,
+D = 7) packed from device-resident ensembles, jittered, searched (kNN + three
+marginal range counts) and reduced to TE values.  Under torchrun each rank
+runs its own C2-sized batch (master seed = rank: distinct surrogates) and the
+per-chunk TE values are all-gathered over NCCL -- weak scaling, whole-job
+value = all ranks' chunks / max-over-ranks step time.
+
+JSON keys beyond the base contract:
+  roofline      dominant kernel, FP32 CUDA-core roofline (not HBM, not tensor:
+                the max-norm is not a contraction).  achieved =
+                2 FP32 ops x algorithmic pair-coordinate evaluations per launch
+                / on-stream launch time (CUDA events inside the library);
+                peak = SMs x 128 lanes x 2 x max SM clock (nominal) with the
+                measured FADD2+FMNMX3 loop ceiling beside it
+  cpu_baseline  the CPU oracle port of the reference sweep (oracle/, OpenMP,
+                all host cores) on a bounded sample of the same chunks
+  e2e           the same metric through the public API analyze_pair() with
+                host numpy ensembles (H2D + D2H inside the timed region)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TE estimates/sec (kNN+range searches/sec alongside)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--surrogates", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def workload(name, surrogates):
+    from paper_1401_4068_b200 import workloads
+    wl = workloads.CONFIGS[name]
+    s = surrogates if surrogates is not None else wl.n_surrogates
+    x, y = wl.ensembles()
+    return wl, s, x, y
+
+
+def items_of(wl, s):
+    return [(u, -1) for u in wl.u_candidates] + [(u, i) for u in wl.u_candidates for i in range(s)]
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self):
+        if self.proc is None or not getattr(self, "lines", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port of the reference sweep; rank 0 only)
+# ---------------------------------------------------------------------------
+def cpu_sample(wl, x, y, budget_s=12.0, max_chunks=16):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    spec = wl.spec
+    u = wl.u_candidates[0]
+    joint = oracle.assemble(x, y, spec, spec, u, wl.window)
+    w = wl.window[1] - wl.window[0] + 1
+    done, t0 = 0, time.perf_counter()
+    while done < max_chunks and (done < 2 or time.perf_counter() - t0 < budget_s):
+        if done == 0:
+            j, seed = joint, np.random.SeedSequence((wl.seed, u, 0))
+        else:
+            perm = oracle.draw_permutation(x.shape[0], np.random.SeedSequence((wl.seed, done - 1)))
+            j = oracle.permuted_joint(joint, perm, w, spec[0])
+            seed = np.random.SeedSequence((wl.seed, u, done))
+        oracle.estimate_te(j, spec[0], spec[0], wl.k, 1e-8, seed)
+        done += 1
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "TE/s", "cores": cores, "kind": "port",
+            "sample": f"{done} chunks of config {wl.name} (u={u}: original + surrogates), "
+                      f"{dt:.1f} s; C oracle (oracle/ente_oracle.c) restating the reference "
+                      "sorted sweep engine.py:70-160 + numpy jitter/digamma, OpenMP"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    wl, s, x, y = workload(args.config, args.surrogates)
+    m = x.shape[0] * (wl.window[1] - wl.window[0] + 1)
+    for _ in range(args.warmup):
+        cpu_sample(wl, x, y, budget_s=0.0, max_chunks=1)
+    t0 = time.perf_counter()
+    samples = [cpu_sample(wl, x, y, budget_s=5.0, max_chunks=8) for _ in range(args.steps)]
+    dt = time.perf_counter() - t0
+    rate = statistics.median([smp["value"] for smp in samples])
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "TE/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference simulators, restated)",
+            "config": {"workload": f"{wl.name}: {wl.description}", "points_per_chunk": m,
+                       "dim": 1 + 2 * wl.spec[0], "k": wl.k},
+            "searches_per_s": rate * m,
+            "cpu_baseline": {**samples[-1], "value": rate},
+            "e2e": {"value": rate, "unit": "TE/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1401_4068_b200 import _native as nat
+    from paper_1401_4068_b200.data import AnalysisConfig, EmbeddingSpec, EnsembleSeries
+    from paper_1401_4068_b200.inference import PairPipeline, analyze_pair, cached_permutation
+    from paper_1401_4068_b200.scheduler import gather_te
+
+    wl, s, x, y = workload(args.config, args.surrogates)
+    spec = EmbeddingSpec(*wl.spec)
+    seed = wl.seed + rank
+    cfg = AnalysisConfig(u_candidates=wl.u_candidates, window=wl.window, k=wl.k, n_surrogates=s,
+                         seed=seed)
+    X, Y = EnsembleSeries("X", x), EnsembleSeries("Y", y)
+    pipe = PairPipeline(X, Y, spec, spec, cfg)
+    perms = [cached_permutation(seed, i, x.shape[0], True) for i in range(s)]
+    pipe.set_perms(perms)
+    items = items_of(wl, s)
+    n_chunks = len(items)
+    m = pipe.m
+    dim = pipe.dim
+
+    def step():
+        te = pipe.run(items)
+        if dist is not None:
+            gather_te(torch.from_numpy(te).cuda(), dist)
+        return te
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    launches0 = nat.launch_count()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk, nat.KernelProfile():
+        start.record()
+        t_wall = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        stop.record()
+        barrier()
+        t_wall = time.perf_counter() - t_wall
+        prof = nat.KernelProfile.read()
+    launches = nat.launch_count() - launches0
+    ms = start.elapsed_time(stop) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = n_chunks * world / (ms * 1e-3)
+
+    # roofline of the dominant kernel (FP32 CUDA-core bound)
+    pce_pass = n_chunks * m * (m - 1) * dim  # per launch: one pass over all ordered pairs
+    dom = max((k for k in prof if k in ("knn_pass", "count_pass")), key=lambda k: prof[k]["ms"])
+    per_launch_ms = prof[dom]["ms"] / max(1, prof[dom]["launches"])
+    achieved = 2.0 * pce_pass / (per_launch_ms * 1e-3) / 1e12
+    props = torch.cuda.get_device_properties(local)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    nominal = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
+    measured_loop = 2.0 * nat.microbench_pce(100) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    total_ms = sum(v["ms"] for v in prof.values())
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
+                "frac": achieved / nominal, "traffic": traffic, "kernel": dom,
+                "peak_kind": f"nominal: {props.multi_processor_count} SMs x 128 lanes x 2 ops x "
+                             f"{sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz); FP32 peak is not in "
+                             "MEASURED_PEAKS.json",
+                "measured_loop_peak": measured_loop,
+                "frac_of_measured_loop": achieved / measured_loop,
+                "kernel_share_of_step": prof[dom]["ms"] / total_ms if total_ms else None,
+                "kernels_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
+                "pce_per_launch": pce_pass,
+                "work_definition": "ordered pairs x columns (n(n-1)D per pass, 2 passes; "
+                                   "SURVEY 8d), 2 FP32 ops per pair-coordinate"}
+
+    # end-to-end through the public API (host ensembles, H2D + D2H in the region)
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(min(2, args.warmup)):
+            analyze_pair(X, Y, spec, spec, cfg)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res = analyze_pair(X, Y, spec, spec, cfg)
+        barrier()
+        e_s = (time.perf_counter() - t0) / args.steps
+        if dist is not None:
+            t = torch.tensor([e_s], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_s = float(t.item())
+        h2d = x.nbytes + y.nbytes + s * x.shape[0] * 4 + n_chunks * (16 + 32)
+        d2h = n_chunks * (8 + 4) + len(res.surrogate_values) * 0
+        e2e = {"value": n_chunks * world / e_s, "unit": "TE/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "api": "paper_1401_4068_b200.analyze_pair"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_sample(wl, x, y)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "TE/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
+                "data": "synthetic: reference simulators restated bit-exactly (workloads.py)",
+                "config": {"workload": f"{wl.name}: {wl.description}", "chunks_per_step": n_chunks,
+                           "points_per_chunk": m, "dim": dim, "k": wl.k, "surrogates": s,
+                           "parallelism": f"dp{world} (chunk sharding, one NCCL all_gather)",
+                           "l2": f"inputs larger than L2: {n_chunks * m * dim * 8 / 1e9:.1f} GB "
+                                 "of joints written and read per step"},
+                "searches_per_s": value * m,
+                "wall_ms_per_step": t_wall / args.steps * 1e3,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": clk.summary(), "gpu_launches": launches}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

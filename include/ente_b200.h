@@ -162,6 +162,29 @@ int ente_te_reduce(const int32_t *counts, int64_t total_rows, const ente_chunk *
                    int n_chunks, const double *psi_table, int64_t table_len, double psi_k,
                    double *out_te, void *workspace, size_t ws_bytes, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Instrumentation (no reference counterpart: the reference only has
+ * time.perf_counter around whole calls, bench.py:71-81).
+ *
+ * ente_launch_count   kernels launched by this library since load
+ * ente_profile_enable when on, every launch is bracketed by CUDA events on
+ *                     its own stream; ente_profile_read synchronises them and
+ *                     returns per-kernel launch counts and total milliseconds
+ *                     (names as consecutive NUL-terminated strings); returns
+ *                     the number of kernels seen
+ * ente_microbench_pce pair-coordinate evaluations per second of the ideal
+ *                     FADD2 + FMNMX3 inner loop (the measured fp32 ceiling)
+ * ------------------------------------------------------------------------- */
+int64_t ente_launch_count(void);
+void ente_profile_enable(int on);
+void ente_profile_reset(void);
+int ente_profile_read(char *names, size_t names_len, int64_t *launches, double *ms,
+                      int max_kernels);
+int ente_microbench_pce(int iters, int blocks, double *pce_per_s, void *stream);
+/* sub-tiles (32 candidates x 128 references) the two sweeps evaluated since
+ * the last call, counted while profiling is on (pruning leaves the rest) */
+void ente_search_work(unsigned long long *knn_subtiles, unsigned long long *count_subtiles);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,6 +51,13 @@ def _declare(L):
         "ente_pack_te": ([vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32p, i32, vp, vp, vp], i32),
         "ente_te_reduce_workspace_size": ([cp, i32], sz),
         "ente_te_reduce": ([vp, i64, cp, i32, vp, i64, dbl, vp, vp, sz, vp], i32),
+        "ente_launch_count": ([], i64),
+        "ente_profile_enable": ([i32], None),
+        "ente_profile_reset": ([], None),
+        "ente_profile_read": ([ctypes.c_char_p, sz, ctypes.POINTER(i64), ctypes.POINTER(dbl), i32],
+                              i32),
+        "ente_microbench_pce": ([i32, i32, ctypes.POINTER(dbl), vp], i32),
+        "ente_search_work": ([ctypes.POINTER(ctypes.c_ulonglong)] * 2, None),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -144,3 +151,45 @@ def pcg_states(seeds, draws_per_seed):
         if isinstance(seed, np.random.Generator):
             gen.bit_generator.advance(int(draws))
     return out
+
+
+def launch_count() -> int:
+    return int(lib().ente_launch_count())
+
+
+class KernelProfile:
+    """Per-kernel on-stream timing of the library's launches (CUDA events)."""
+
+    def __enter__(self):
+        lib().ente_profile_reset()
+        lib().ente_profile_enable(1)
+        return self
+
+    def __exit__(self, *exc):
+        lib().ente_profile_enable(0)
+        return False
+
+    @staticmethod
+    def read() -> dict:
+        L = lib()
+        cap = 64
+        names = ctypes.create_string_buffer(4096)
+        launches = (ctypes.c_int64 * cap)()
+        ms = (ctypes.c_double * cap)()
+        n = L.ente_profile_read(names, len(names), launches, ms, cap)
+        keys = [k.decode() for k in names.raw.split(b"\0")[:n]]
+        return {k: {"launches": int(launches[i]), "ms": float(ms[i])} for i, k in enumerate(keys)}
+
+
+def microbench_pce(iters: int = 200) -> float:
+    out = ctypes.c_double()
+    check(lib().ente_microbench_pce(int(iters), 0, ctypes.byref(out), stream_handle()),
+          "ente_microbench_pce")
+    return out.value
+
+
+def search_work() -> tuple[int, int]:
+    """(knn, count) sub-tiles evaluated since the last call (profiling on)."""
+    a, b = ctypes.c_ulonglong(), ctypes.c_ulonglong()
+    lib().ente_search_work(ctypes.byref(a), ctypes.byref(b))
+    return int(a.value), int(b.value)

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "profile.cuh"
 
 namespace ente {
 
@@ -223,15 +224,17 @@ extern "C" int ente_jitter(double *pts64, int dim, const ente_chunk *chunks, int
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ENTE_CUDA(cudaMemcpyAsync(w.ch, h.data(), sizeof(JitChunk) * n_chunks, cudaMemcpyHostToDevice, st));
     if (amplitude > 0) {
-        jitter_std_kernel<<<n_chunks, 32, 0, st>>>(pts64, dim, w.ch, amplitude, w.hw);
+        ENTE_LAUNCH("jitter_std", st,
+                    jitter_std_kernel<<<n_chunks, 32, 0, st>>>(pts64, dim, w.ch, amplitude, w.hw));
         ENTE_CUDA(cudaGetLastError());
         const int64_t per_block = 256LL * kJitPerThread;
         const int64_t gx = ((int64_t)max_n * dim + per_block - 1) / per_block;
         dim3 grid((unsigned)gx, (unsigned)n_chunks);
-        jitter_apply_kernel<<<grid, 256, 0, st>>>(pts64, dim, w.ch, w.hw);
+        ENTE_LAUNCH("jitter_apply", st,
+                    jitter_apply_kernel<<<grid, 256, 0, st>>>(pts64, dim, w.ch, w.hw));
         ENTE_CUDA(cudaGetLastError());
     }
-    check_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.ch, status);
+    ENTE_LAUNCH("check", st, check_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.ch, status));
     ENTE_CUDA(cudaGetLastError());
     return ENTE_OK;
 }

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "profile.cuh"
 
 namespace ente {
 
@@ -76,8 +77,9 @@ extern "C" int ente_pack_te(const double *x, const double *y, int reps, int n_sa
     ENTE_CUDA(cudaMemcpyAsync(ditems, items, sizeof(PackItem) * n_items, cudaMemcpyHostToDevice, st));
     const int64_t rows = (int64_t)reps * w;
     dim3 grid((unsigned)((rows + 255) / 256), (unsigned)n_items);
-    pack_te_kernel<<<grid, 256, 0, st>>>(x, y, reps, n_samples, dx, tau_x, dy, tau_y, t_lo, w, ditems,
-                                         perms, out);
+    ENTE_LAUNCH("pack_te", st,
+                pack_te_kernel<<<grid, 256, 0, st>>>(x, y, reps, n_samples, dx, tau_x, dy, tau_y,
+                                                     t_lo, w, ditems, perms, out));
     ENTE_CUDA(cudaGetLastError());
     ENTE_CUDA(cudaFreeAsync(ditems, st));
     return ENTE_OK;

@@ -6,8 +6,15 @@
 // exact fp64 answer is produced by an fp32 filter with a proven error bound
 // and fp64 certification of the few pairs the filter cannot decide:
 //
-//   prep      centre each chunk, fp32 copy x32 = fl32(x - m), bound
+//   prep      column mean / min / max, bound
 //             delta = 4 * 2^-24 * max|x - m| * (1 + 2^-20) >= |d32 - d64|
+//   sort      per-chunk Morton order over the filter columns (the y-past
+//             block: every contribution needs max|dy-past| inside the radius),
+//             CTA radix sort; fp32 copy x32 = fl32(x - m) in that order plus
+//             per-32 / per-128-row bounding boxes
+//   pruning   a warp (128 sorted references) skips a 32-candidate sub-tile
+//             when the fp32 box distance already exceeds its bound; boxes are
+//             exact lower bounds of every d32 in them, so skipping is exact
 //   pass 1    t32_i = k-th smallest fp32 distance (self excluded) via a
 //             (k+1)-slot sorted register list; L_i = #{d32 < lo_i}
 //   pass 2    per pair: the three TE marginal distances and the joint one;
@@ -27,53 +34,66 @@
 #include <vector>
 
 #include "common.cuh"
+#include "profile.cuh"
+#include "radix.cuh"
 
 namespace ente {
 
 // ---------------------------------------------------------------------------
-// prep: centring, fp32 copy, error bound, finiteness
+// prep: column statistics, error bound, finiteness
 // ---------------------------------------------------------------------------
+constexpr int kSub = 32;                    // rows per sub-tile box (one warp of candidates)
+constexpr int kSubPerStage = kTJ / kSub;    // sub-tiles per shared-memory stage
+constexpr int kWarps = kNT / 32;            // warps per sweep CTA; warp w owns 128 refs
+
+// per-chunk column statistics (fp64): mean, min, max of the raw values
+struct ColStats {
+    double mean[kMaxDim];
+    double lo[kMaxDim];
+    double hi[kMaxDim];
+};
+
 __global__ void __launch_bounds__(256) prep_kernel(const double *__restrict__ pts64, int dim,
                                                    ChunkInfo *__restrict__ info,
-                                                   float *__restrict__ pts32, int dp,
-                                                   int32_t *__restrict__ status, int write32) {
+                                                   ColStats *__restrict__ stats,
+                                                   int32_t *__restrict__ status, int want32) {
     const int c = blockIdx.x;
-    ChunkInfo ci = info[c];
+    const ChunkInfo ci = info[c];
     if (status[c] != ENTE_CHUNK_OK) return;
-    __shared__ double red[256];
-    __shared__ double mean[kMaxDim];
+    __shared__ double red[3][256];
+    __shared__ ColStats local;
     __shared__ int bad;
     if (threadIdx.x == 0) bad = 0;
     const double *p = pts64 + ci.row0 * dim;
-    const int64_t cnt = (int64_t)ci.n * dim;
-    // column sums (any order: the centre only has to be some fp64 value)
+    ColStats *cs = &local;
     for (int col = 0; col < dim; ++col) {
-        double s = 0.0;
-        for (int r = threadIdx.x; r < ci.n; r += blockDim.x) s += p[(int64_t)r * dim + col];
-        red[threadIdx.x] = s;
+        double s = 0.0, lo = INFINITY, hi = -INFINITY;
+        for (int r = threadIdx.x; r < ci.n; r += blockDim.x) {
+            const double v = p[(int64_t)r * dim + col];
+            s += v;
+            lo = fmin(lo, v);
+            hi = fmax(hi, v);
+            if (!isfinite(v)) bad = 1;
+        }
+        red[0][threadIdx.x] = s;
+        red[1][threadIdx.x] = lo;
+        red[2][threadIdx.x] = hi;
         __syncthreads();
         for (int w = 128; w > 0; w >>= 1) {
-            if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+            if (threadIdx.x < w) {
+                red[0][threadIdx.x] += red[0][threadIdx.x + w];
+                red[1][threadIdx.x] = fmin(red[1][threadIdx.x], red[1][threadIdx.x + w]);
+                red[2][threadIdx.x] = fmax(red[2][threadIdx.x], red[2][threadIdx.x + w]);
+            }
             __syncthreads();
         }
-        if (threadIdx.x == 0) mean[col] = red[0] / ci.n;
+        if (threadIdx.x == 0) {
+            cs->mean[col] = red[0][0] / ci.n;
+            cs->lo[col] = red[1][0];
+            cs->hi[col] = red[2][0];
+        }
         __syncthreads();
     }
-    // spread s = max |fl64(x - m)|, finiteness
-    double smax = 0.0;
-    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
-        double v = p[e];
-        if (!isfinite(v)) bad = 1;
-        double dv = fabs(__dsub_rn(v, mean[e % dim]));
-        smax = fmax(smax, dv);
-    }
-    red[threadIdx.x] = smax;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
-        __syncthreads();
-    }
-    smax = red[0];
     if (bad) {
         if (threadIdx.x == 0) {
             status[c] = ENTE_CHUNK_NONFINITE;
@@ -81,23 +101,126 @@ __global__ void __launch_bounds__(256) prep_kernel(const double *__restrict__ pt
         }
         return;
     }
-    // the fp32 path needs normal-range fp32 values
-    const int ok = (smax > 1e-30) && (smax < 1e30);
-    if (threadIdx.x == 0) {
+    if (stats)
+        for (int e = threadIdx.x; e < 3 * kMaxDim; e += blockDim.x)
+            (&stats[c].mean[0])[e] = (&local.mean[0])[e];
+    if (threadIdx.x == 0 && stats) {
+        // spread s = max |fl64(x - m)| is attained at a column extreme
+        double smax = 0.0;
+        for (int col = 0; col < dim; ++col) {
+            smax = fmax(smax, fabs(__dsub_rn(cs->lo[col], cs->mean[col])));
+            smax = fmax(smax, fabs(__dsub_rn(cs->hi[col], cs->mean[col])));
+        }
+        // the fp32 path needs normal-range fp32 values
+        const int ok = (smax > 1e-30) && (smax < 1e30);
         info[c].delta = 4.0 * 0x1p-24 * smax * (1.0 + 0x1p-20);
-        info[c].ok32 = ok && write32;
+        info[c].ok32 = ok && want32;
     }
-    if (!(ok && write32)) return;
-    float *q = pts32 + ci.prow0 * dp;
-    const int64_t pcnt = (int64_t)ci.npad * dp;
-    for (int64_t e = threadIdx.x; e < pcnt; e += blockDim.x) {
-        int64_t r = e / dp;
-        int col = (int)(e - r * dp);
-        float v;
-        if (r >= ci.n) v = INFINITY;
-        else if (col >= dim) v = 0.0f;
-        else v = __double2float_rn(__dsub_rn(p[r * dim + col], mean[col]));
-        q[e] = v;
+}
+
+// ---------------------------------------------------------------------------
+// sort: Morton order over the filter columns [f0, f0 + nf), stable radix
+// ---------------------------------------------------------------------------
+struct FilterCols {
+    int f0, nf, bits;  // columns and Morton bits per column
+};
+
+__global__ void __launch_bounds__(kSortThreads) sort_kernel(
+    const double *__restrict__ pts64, int dim, const ChunkInfo *__restrict__ info,
+    const ColStats *__restrict__ stats, FilterCols fc, uint32_t *__restrict__ ka,
+    uint32_t *__restrict__ kb, int32_t *__restrict__ va, int32_t *__restrict__ vb,
+    int32_t *__restrict__ perm) {
+    __shared__ SortSmem sm;
+    __shared__ double qlo[kMaxDim], qscale[kMaxDim];
+    const ChunkInfo ci = info[blockIdx.x];
+    if (!ci.ok32) return;
+    const ColStats *cs = stats + blockIdx.x;
+    const uint32_t qmax = (1u << fc.bits) - 1u;
+    if (threadIdx.x < fc.nf) {
+        const int col = fc.f0 + threadIdx.x;
+        const double span = cs->hi[col] - cs->lo[col];
+        qlo[threadIdx.x] = cs->lo[col];
+        qscale[threadIdx.x] = span > 0.0 ? (double)qmax / span : 0.0;
+    }
+    __syncthreads();
+    const double *p = pts64 + ci.row0 * dim;
+    uint32_t *k0 = ka + ci.row0, *k1 = kb + ci.row0;
+    int32_t *v0 = va + ci.row0, *v1 = vb + ci.row0;
+    for (int i = threadIdx.x; i < ci.n; i += kSortThreads) {
+        uint32_t key = 0;
+        uint32_t q[kMaxDim];
+        for (int f = 0; f < fc.nf; ++f) {
+            const double t = (p[(int64_t)i * dim + fc.f0 + f] - qlo[f]) * qscale[f];
+            q[f] = (uint32_t)fmin(fmax(t, 0.0), (double)qmax);
+        }
+        for (int b = fc.bits - 1; b >= 0; --b)
+            for (int f = 0; f < fc.nf; ++f) key = (key << 1) | ((q[f] >> b) & 1u);
+        k0[i] = key;
+        v0[i] = i;
+    }
+    __syncthreads();
+    const int par = cta_radix_sort<uint32_t, int32_t>(k0, k1, v0, v1, ci.n, fc.nf * fc.bits, sm);
+    const int32_t *res = par ? v1 : v0;
+    for (int i = threadIdx.x; i < ci.n; i += kSortThreads) perm[ci.row0 + i] = res[i];
+}
+
+// ---------------------------------------------------------------------------
+// gather: sorted fp32 rows (centred) + bounding boxes per 32 and 128 rows
+// box layout: [lo[0..dp) | hi[0..dp)] per tile
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTJ) gather_kernel(const double *__restrict__ pts64, int dim,
+                                                     const ChunkInfo *__restrict__ info, int n_chunks,
+                                                     const ColStats *__restrict__ stats,
+                                                     const int32_t *__restrict__ perm, int dp,
+                                                     float *__restrict__ pts32,
+                                                     float *__restrict__ box32,
+                                                     float *__restrict__ box128) {
+    __shared__ float slo[kTJ / 32][kMaxDim], shi[kTJ / 32][kMaxDim];
+    for (int cidx = blockIdx.y; cidx < n_chunks; cidx += gridDim.y) {
+    const ChunkInfo ci = info[cidx];
+    const int stage = blockIdx.x;
+    if (!ci.ok32 || stage * kTJ >= ci.npad) continue;
+    const ColStats *cs = stats + cidx;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int s = stage * kTJ + threadIdx.x;
+    const bool valid = s < ci.n;
+    const int64_t orig = valid ? ci.row0 + perm[ci.row0 + s] : 0;
+    float *q = pts32 + (ci.prow0 + s) * dp;
+    const int64_t sub = ci.prow0 / kSub + stage * kSubPerStage + warp;
+    for (int col = 0; col < dp; ++col) {
+        float v = 0.0f;
+        if (col < dim)
+            v = valid ? __double2float_rn(__dsub_rn(pts64[orig * dim + col], cs->mean[col])) : INFINITY;
+        q[col] = v;
+        float lo = (valid && col < dim) ? v : INFINITY;
+        float hi = (valid && col < dim) ? v : -INFINITY;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+        }
+        if (lane == 0) {
+            box32[sub * 2 * dp + col] = lo;
+            box32[sub * 2 * dp + dp + col] = hi;
+            if (col < kMaxDim) {
+                slo[warp][col] = lo;
+                shi[warp][col] = hi;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < dp) {
+        const int col = threadIdx.x;
+        float lo = INFINITY, hi = -INFINITY;
+        for (int w = 0; w < kTJ / 32; ++w) {
+            lo = fminf(lo, slo[w][col]);
+            hi = fmaxf(hi, shi[w][col]);
+        }
+        const int64_t t = ci.prow0 / kTJ + stage;
+        box128[t * 2 * dp + col] = lo;
+        box128[t * 2 * dp + dp + col] = hi;
+    }
+    __syncthreads();
     }
 }
 
@@ -192,85 +315,6 @@ __device__ __forceinline__ void ring_issue(Ring<DP> &ring, int stage, const floa
     bulk_g2s(ring.buf[stage], src, bytes, &ring.full[stage]);
 }
 
-// ---------------------------------------------------------------------------
-// pass 1: fp32 k-th neighbour distance (self included as the (k+1)-th slot)
-// ---------------------------------------------------------------------------
-template <int D, int S>
-__global__ void __launch_bounds__(kNT) knn_pass_kernel(const float *__restrict__ pts32,
-                                                       const ChunkInfo *__restrict__ info,
-                                                       const TileRef *__restrict__ tiles, int k,
-                                                       float *__restrict__ t32_out,
-                                                       int32_t *__restrict__ L_out) {
-    constexpr int DP = (D + 3) & ~3;
-    __shared__ __align__(128) Ring<DP> ring;
-    const TileRef tr = tiles[blockIdx.x];
-    const ChunkInfo ci = info[tr.chunk];
-    if (!ci.ok32) return;
-    const float *cp = pts32 + ci.prow0 * DP;
-    const int ntile = ci.npad / kTJ;
-    if (threadIdx.x == 0) {
-        mbar_init(&ring.full[0], 1);
-        mbar_init(&ring.full[1], 1);
-        fence_barrier_init();
-        ring_issue(ring, 0, cp);
-        if (ntile > 1) ring_issue(ring, 1, cp + kTJ * DP);
-    }
-    Ref<D> ref[kRT];
-    float kd[kRT][S];
-#pragma unroll
-    for (int r = 0; r < kRT; ++r) {
-        const int idx = tr.r0 + r * kNT + threadIdx.x;
-        load_ref<D>(ref[r], cp + (int64_t)idx * DP, idx < ci.n);
-#pragma unroll
-        for (int s = 0; s < S; ++s) kd[r][s] = (s < S - (k + 1)) ? -INFINITY : INFINITY;
-    }
-    __syncthreads();
-    for (int t = 0; t < ntile; ++t) {
-        const int st = t & 1;
-        mbar_wait(&ring.full[st], (t >> 1) & 1);
-        const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[st]);
-#pragma unroll 2
-        for (int j = 0; j < kTJ; ++j) {
-            Cand<D> c;
-#pragma unroll
-            for (int q = 0; q < DP / 4; ++q) c.v[q] = tile[j * (DP / 4) + q];
-            float d[kRT];
-            bool any = false;
-#pragma unroll
-            for (int r = 0; r < kRT; ++r) {
-                float a[D];
-                diffs<D>(ref[r], c, a);
-                d[r] = maxabs0<0, D, D>(a);
-                any |= d[r] < kd[r][S - 1];
-            }
-            if (any) {
-#pragma unroll
-                for (int r = 0; r < kRT; ++r) insert_sorted<S>(kd[r], d[r]);
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0 && t + 2 < ntile) ring_issue(ring, st, cp + (int64_t)(t + 2) * kTJ * DP);
-    }
-#pragma unroll
-    for (int r = 0; r < kRT; ++r) {
-        const int idx = tr.r0 + r * kNT + threadIdx.x;
-        if (idx >= ci.n) continue;
-        const float t32 = kd[r][S - 1];
-        const float lo = __double2float_rd(__dsub_rd((double)t32, 2.0 * ci.delta));
-        int L = 0;
-#pragma unroll
-        for (int s = 0; s < S; ++s) L += (kd[r][s] > -INFINITY) && (kd[r][s] < lo);
-        if (lo > 0.0f) L -= 1;  // the self pair (distance 0) was counted
-        t32_out[ci.row0 + idx] = t32;
-        L_out[ci.row0 + idx] = L;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// pass 2: certain counts in the three TE marginals + band events
-//   columns: 0 = y_t, 1..DY = y-past, DY+1..D-1 = x-past (embedding.py:50-60)
-//   marginal 0 = y-past (A), 1 = y + y-past, 2 = y-past + x-past
-// ---------------------------------------------------------------------------
 struct Band {
     float nlo, nt;  // -lo, -t
     float lo, hi, w;
@@ -290,120 +334,379 @@ __device__ __forceinline__ Band make_band(float t32, double delta) {
     return b;
 }
 
-template <int DY, int DX>
-__global__ void __launch_bounds__(kNT) count_pass_kernel(
-    const float *__restrict__ pts32, const ChunkInfo *__restrict__ info,
-    const TileRef *__restrict__ tiles, const float *__restrict__ t32_in, int64_t total_rows,
-    int32_t *__restrict__ cnt_out, uint32_t *__restrict__ ev, int32_t *__restrict__ ev_n,
-    uint32_t fmask) {
-    constexpr int D = 1 + DY + DX;
+// ---------------------------------------------------------------------------
+// traversal: candidate stages visited home-first, then alternately below and
+// above (spatially nearest first in the Morton order, so kNN bounds shrink
+// early); warp 0 evaluates 32 positions at a time and picks the first stage
+// some warp still needs (its box distance below that warp's bound)
+// ---------------------------------------------------------------------------
+struct Trav {
+    int h0, nh, nst, npos;
+    __device__ void init(int r0, int n, int npad) {
+        h0 = r0 / kTJ;
+        nh = (min(r0 + kRefTile, n) - r0 + kTJ - 1) / kTJ;
+        nst = npad / kTJ;
+        npos = nh + 2 * max(h0, nst - h0 - nh);
+    }
+    __device__ int stage_at(int pos) const {
+        if (pos < nh) return h0 + pos;
+        const int p = pos - nh, k = (p >> 1) + 1;
+        const int s = (p & 1) ? h0 + nh - 1 + k : h0 - k;
+        return (s >= 0 && s < nst) ? s : -1;
+    }
+};
+
+// fp32 box distance over columns [c0, c1): a lower bound of every d32 between
+// the two boxes (fl is monotone: fl(x_j - x_i) >= fl(lo_j - hi_i))
+template <int DP>
+__device__ __forceinline__ float box_dist(const float *a, const float *b, int c0, int c1) {
+    float m = 0.0f;
+#pragma unroll
+    for (int c = 0; c < DP; ++c) {
+        if (c < c0 || c >= c1) continue;
+        m = fmaxf(m, fmaxf(b[c] - a[DP + c], a[c] - b[DP + c]));
+    }
+    return m;
+}
+
+__device__ __forceinline__ float warp_max_nonneg(float v) {
+    return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(v, 0.0f))));
+}
+
+// Warp 0: next stage to load (or -1).  strict: process iff dist < bound (kNN);
+// otherwise iff dist <= bound (counts: the band is closed at hi).
+template <int DP>
+__device__ __forceinline__ int next_stage(const Trav &tv, int &spos, const float *box128,
+                                          int64_t stage0, const float (*wbox)[2 * DP],
+                                          const float *wbound, int c0, int c1, bool strict,
+                                          int prune) {
+    const int lane = threadIdx.x & 31;
+    while (spos < tv.npos) {
+        const int pos = spos + lane;
+        const int st = pos < tv.npos ? tv.stage_at(pos) : -1;
+        bool take = false;
+        if (st >= 0) {
+            if (!prune) {
+                take = true;
+            } else {
+                const float *bb = box128 + (stage0 + st) * 2 * DP;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) {
+                    const float d = box_dist<DP>(wbox[w], bb, c0, c1);
+                    take |= strict ? (d < wbound[w]) : (d <= wbound[w]);
+                }
+            }
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, take);
+        if (hit) {
+            const int first = __ffs(hit) - 1;
+            spos += first + 1;
+            return __shfl_sync(0xffffffffu, st, first);
+        }
+        spos += 32;
+    }
+    return -1;
+}
+
+// ---------------------------------------------------------------------------
+// pass 1: fp32 k-th neighbour distance (self included as the (k+1)-th slot)
+// refs: warp w owns sorted rows r0 + w*128 + r*32 + lane, r < kRT
+// ---------------------------------------------------------------------------
+template <int D, int S>
+__global__ void __launch_bounds__(kNT) knn_pass_kernel(
+    const float *__restrict__ pts32, const float *__restrict__ box32,
+    const float *__restrict__ box128, const ChunkInfo *__restrict__ info,
+    const TileRef *__restrict__ tiles, int k, int prune, float *__restrict__ t32_out,
+    int32_t *__restrict__ L_out, unsigned long long *__restrict__ work) {
     constexpr int DP = (D + 3) & ~3;
     __shared__ __align__(128) Ring<DP> ring;
+    __shared__ float wbox[kWarps][2 * DP];
+    __shared__ float wbound[kWarps];
+    __shared__ int sid[2];
     const TileRef tr = tiles[blockIdx.x];
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float *cp = pts32 + ci.prow0 * DP;
-    const int ntile = ci.npad / kTJ;
+    const int64_t sub0 = ci.prow0 / kSub, stage0 = ci.prow0 / kTJ;
+    Trav tv;
+    tv.init(tr.r0, ci.n, ci.npad);
+    const int wrow = tr.r0 + warp * kTJ;  // first sorted row of this warp
+    const bool wvalid = wrow < ci.n;
+    for (int e = lane; e < 2 * DP; e += 32)
+        wbox[warp][e] = wvalid ? box128[(stage0 + wrow / kTJ) * 2 * DP + e]
+                               : (e < DP ? INFINITY : -INFINITY);
+    if (lane == 0) wbound[warp] = wvalid ? INFINITY : 0.0f;
+    Ref<D> ref[kRT];
+    float kd[kRT][S];
+#pragma unroll
+    for (int r = 0; r < kRT; ++r) {
+        const int idx = wrow + r * 32 + lane;
+        const bool valid = idx < ci.n;
+        load_ref<D>(ref[r], cp + (int64_t)idx * DP, valid);
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            kd[r][s] = (!valid || s < S - (k + 1)) ? -INFINITY : INFINITY;
+    }
     if (threadIdx.x == 0) {
         mbar_init(&ring.full[0], 1);
         mbar_init(&ring.full[1], 1);
         fence_barrier_init();
-        ring_issue(ring, 0, cp);
-        if (ntile > 1) ring_issue(ring, 1, cp + kTJ * DP);
     }
-    Ref<D> ref[kRT];
-    Band band[kRT];
-    uint32_t c0[kRT], c1[kRT], c2[kRT];
-    int nev[kRT];
+    __syncthreads();
+    int spos = 0;
+    if (warp == 0) {
+        for (int b = 0; b < 2; ++b) {
+            const int st = next_stage<DP>(tv, spos, box128, stage0, wbox, wbound, 0, D, true, prune);
+            if (lane == 0) {
+                sid[b] = st;
+                if (st >= 0) ring_issue(ring, b, cp + (int64_t)st * kTJ * DP);
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t uses = 0;  // bit b: parity of buffer b
+    uint32_t nsub = 0;  // sub-tiles this warp evaluated
+    for (int it = 0;; ++it) {
+        const int b = it & 1;
+        const int cur = sid[b];
+        if (cur < 0) break;
+        mbar_wait(&ring.full[b], (uses >> b) & 1u);
+        uses ^= 1u << b;
+        const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[b]);
+        for (int q = 0; q < kSubPerStage; ++q) {
+            if (prune) {
+                float wb = 0.0f;
+#pragma unroll
+                for (int r = 0; r < kRT; ++r) wb = fmaxf(wb, kd[r][S - 1]);
+                wb = warp_max_nonneg(wb);
+                const float bd = box_dist<DP>(wbox[warp], box32 + (sub0 + (int64_t)cur * kSubPerStage + q) * 2 * DP, 0, D);
+                if (!(bd < wb)) continue;
+            }
+            ++nsub;
+#pragma unroll 2
+            for (int jj = 0; jj < kSub; ++jj) {
+                const int j = q * kSub + jj;
+                Cand<D> c;
+#pragma unroll
+                for (int v = 0; v < DP / 4; ++v) c.v[v] = tile[j * (DP / 4) + v];
+                float d[kRT];
+                bool any = false;
+#pragma unroll
+                for (int r = 0; r < kRT; ++r) {
+                    float a[D];
+                    diffs<D>(ref[r], c, a);
+                    d[r] = maxabs0<0, D, D>(a);
+                    any |= d[r] < kd[r][S - 1];
+                }
+                if (any) {
+#pragma unroll
+                    for (int r = 0; r < kRT; ++r) insert_sorted<S>(kd[r], d[r]);
+                }
+            }
+        }
+        {
+            float wb = 0.0f;
+#pragma unroll
+            for (int r = 0; r < kRT; ++r) wb = fmaxf(wb, kd[r][S - 1]);
+            wb = warp_max_nonneg(wb);
+            if (lane == 0 && wvalid) wbound[warp] = wb;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int st = next_stage<DP>(tv, spos, box128, stage0, wbox, wbound, 0, D, true, prune);
+            if (lane == 0) {
+                sid[b] = st;
+                if (st >= 0) ring_issue(ring, b, cp + (int64_t)st * kTJ * DP);
+            }
+        }
+        __syncthreads();
+    }
+    if (lane == 0 && wvalid) atomicAdd(work, (unsigned long long)nsub);
 #pragma unroll
     for (int r = 0; r < kRT; ++r) {
-        const int idx = tr.r0 + r * kNT + threadIdx.x;
+        const int idx = wrow + r * 32 + lane;
+        if (idx >= ci.n) continue;
+        const float t32 = kd[r][S - 1];
+        const float lo = __double2float_rd(__dsub_rd((double)t32, 2.0 * ci.delta));
+        int L = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) L += (kd[r][s] > -INFINITY) && (kd[r][s] < lo);
+        if (lo > 0.0f) L -= 1;  // the self pair (distance 0) was counted
+        t32_out[ci.row0 + idx] = t32;
+        L_out[ci.row0 + idx] = L;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// pass 2: certain counts in the three TE marginals + band events
+//   columns: 0 = y_t, 1..DY = y-past, DY+1..D-1 = x-past (embedding.py:50-60)
+//   marginal 0 = y-past (A), 1 = y + y-past, 2 = y-past + x-past
+//   pruning uses the filter columns [f0, f0 + nf): a subset of every
+//   requested marginal and of the joint, so their box distance bounds all
+//   values that can count or fall in the band
+// ---------------------------------------------------------------------------
+template <int DY, int DX>
+__global__ void __launch_bounds__(kNT) count_pass_kernel(
+    const float *__restrict__ pts32, const float *__restrict__ box32,
+    const float *__restrict__ box128, const ChunkInfo *__restrict__ info,
+    const TileRef *__restrict__ tiles, const float *__restrict__ t32_in, int64_t ws_rows,
+    FilterCols fc, int prune, int32_t *__restrict__ cnt_out, uint32_t *__restrict__ ev,
+    int32_t *__restrict__ ev_n, uint32_t fmask, unsigned long long *__restrict__ work) {
+    constexpr int D = 1 + DY + DX;
+    constexpr int DP = (D + 3) & ~3;
+    __shared__ __align__(128) Ring<DP> ring;
+    __shared__ float wbox[kWarps][2 * DP];
+    __shared__ float wbound[kWarps];
+    __shared__ int sid[2];
+    const TileRef tr = tiles[blockIdx.x];
+    const ChunkInfo ci = info[tr.chunk];
+    if (!ci.ok32) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float *cp = pts32 + ci.prow0 * DP;
+    const int64_t sub0 = ci.prow0 / kSub, stage0 = ci.prow0 / kTJ;
+    const int c0 = fc.f0, c1 = fc.f0 + fc.nf;
+    Trav tv;
+    tv.init(tr.r0, ci.n, ci.npad);
+    const int wrow = tr.r0 + warp * kTJ;
+    const bool wvalid = wrow < ci.n;
+    for (int e = lane; e < 2 * DP; e += 32)
+        wbox[warp][e] = wvalid ? box128[(stage0 + wrow / kTJ) * 2 * DP + e]
+                               : (e < DP ? INFINITY : -INFINITY);
+    Ref<D> ref[kRT];
+    Band band[kRT];
+    uint32_t cA[kRT], c2[kRT], c3[kRT];
+    int nev[kRT];
+    float hmax = 0.0f;
+#pragma unroll
+    for (int r = 0; r < kRT; ++r) {
+        const int idx = wrow + r * 32 + lane;
         const bool valid = idx < ci.n;
         load_ref<D>(ref[r], cp + (int64_t)idx * DP, valid);
-        // invalid lanes get an empty band (never inside, never an event)
-        band[r] = make_band(valid ? t32_in[ci.row0 + idx] : -1.0f, ci.delta);
-        if (!valid) {
+        band[r] = make_band(valid ? t32_in[ci.row0 + idx] : 0.0f, ci.delta);
+        if (!valid) {  // empty band: never inside, never an event
             band[r].lo = -INFINITY;
             band[r].nlo = INFINITY;
             band[r].hi = -INFINITY;
             band[r].w = -1.0f;
+        } else {
+            hmax = fmaxf(hmax, band[r].hi);
         }
-        c0[r] = c1[r] = c2[r] = 0;
+        cA[r] = c2[r] = c3[r] = 0;
         nev[r] = 0;
     }
+    const float wb = warp_max_nonneg(hmax);
+    if (lane == 0) wbound[warp] = wvalid ? wb : -1.0f;
+    if (threadIdx.x == 0) {
+        mbar_init(&ring.full[0], 1);
+        mbar_init(&ring.full[1], 1);
+        fence_barrier_init();
+    }
     __syncthreads();
-    for (int t = 0; t < ntile; ++t) {
-        const int st = t & 1;
-        mbar_wait(&ring.full[st], (t >> 1) & 1);
-        const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[st]);
-#pragma unroll 1
-        for (int j = 0; j < kTJ; ++j) {
-            Cand<D> c;
-#pragma unroll
-            for (int q = 0; q < DP / 4; ++q) c.v[q] = tile[j * (DP / 4) + q];
-            float vA[kRT], v2[kRT], v3[kRT], vj[kRT];
-            bool any = false;
-#pragma unroll
-            for (int r = 0; r < kRT; ++r) {
-                float a[D];
-                diffs<D>(ref[r], c, a);
-                const float A = maxabs0<1, 1 + DY, D>(a);
-                const float m2 = fmaxf(A, fabsf(a[0]));
-                const float m3 = maxabs<1 + DY, D, D>(a, A);
-                const float jd = fmaxf(m2, m3);
-                // certain-inside counts: sign bit of (v - lo)
-                const float2 e = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nlo, band[r].nlo));
-                const float e3 = m3 + band[r].nlo;
-                c0[r] += __float_as_uint(e.x) >> 31;
-                c1[r] += __float_as_uint(e.y) >> 31;
-                c2[r] += __float_as_uint(e3) >> 31;
-                // conservative band test: min |v - t| <= w
-                const float2 b1 = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nt, band[r].nt));
-                const float2 b2 = __fadd2_rn(make_float2(m3, jd), make_float2(band[r].nt, band[r].nt));
-                const float bm = fminf(fminf(fabsf(b1.x), fabsf(b1.y)), fminf(fabsf(b2.x), fabsf(b2.y)));
-                any |= bm <= band[r].w;
-                vA[r] = A;
-                v2[r] = m2;
-                v3[r] = m3;
-                vj[r] = jd;
+    int spos = 0;
+    if (warp == 0) {
+        for (int b = 0; b < 2; ++b) {
+            const int st = next_stage<DP>(tv, spos, box128, stage0, wbox, wbound, c0, c1, false, prune);
+            if (lane == 0) {
+                sid[b] = st;
+                if (st >= 0) ring_issue(ring, b, cp + (int64_t)st * kTJ * DP);
             }
-            if (any) {
-                const int jg = t * kTJ + j;
+        }
+    }
+    __syncthreads();
+    uint32_t uses = 0;
+    uint32_t nsub = 0;
+    for (int it = 0;; ++it) {
+        const int b = it & 1;
+        const int cur = sid[b];
+        if (cur < 0) break;
+        mbar_wait(&ring.full[b], (uses >> b) & 1u);
+        uses ^= 1u << b;
+        const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[b]);
+        for (int q = 0; q < kSubPerStage; ++q) {
+            if (prune) {
+                const float bd = box_dist<DP>(wbox[warp], box32 + (sub0 + (int64_t)cur * kSubPerStage + q) * 2 * DP, c0, c1);
+                if (!(bd <= wb) || !wvalid) continue;
+            }
+            ++nsub;
+#pragma unroll 1
+            for (int jj = 0; jj < kSub; ++jj) {
+                const int j = q * kSub + jj;
+                Cand<D> c;
+#pragma unroll
+                for (int v = 0; v < DP / 4; ++v) c.v[v] = tile[j * (DP / 4) + v];
+                float vA[kRT], v2[kRT], v3[kRT], vj[kRT];
+                bool any = false;
 #pragma unroll
                 for (int r = 0; r < kRT; ++r) {
-                    const float lo = band[r].lo, hi = band[r].hi;
-                    uint32_t f = ((vA[r] >= lo && vA[r] <= hi) ? 1u : 0u) |
-                                 ((v2[r] >= lo && v2[r] <= hi) ? 2u : 0u) |
-                                 ((v3[r] >= lo && v3[r] <= hi) ? 4u : 0u) |
-                                 ((vj[r] >= lo && vj[r] <= hi) ? 8u : 0u);
-                    f &= fmask;
-                    if (f) {
-                        const int idx = tr.r0 + r * kNT + threadIdx.x;
-                        if (nev[r] < kCap)
-                            ev[(ci.row0 + idx) * kCap + nev[r]] = (uint32_t)jg | (f << 28);
-                        ++nev[r];
+                    float a[D];
+                    diffs<D>(ref[r], c, a);
+                    const float A = maxabs0<1, 1 + DY, D>(a);
+                    const float m2 = fmaxf(A, fabsf(a[0]));
+                    const float m3 = maxabs<1 + DY, D, D>(a, A);
+                    const float jd = fmaxf(m2, m3);
+                    // certain-inside counts: sign bit of (v - lo)
+                    const float2 e = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nlo, band[r].nlo));
+                    const float e3 = m3 + band[r].nlo;
+                    cA[r] += __float_as_uint(e.x) >> 31;
+                    c2[r] += __float_as_uint(e.y) >> 31;
+                    c3[r] += __float_as_uint(e3) >> 31;
+                    // conservative band test: min |v - t| <= w
+                    const float2 b1 = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nt, band[r].nt));
+                    const float2 b2 = __fadd2_rn(make_float2(m3, jd), make_float2(band[r].nt, band[r].nt));
+                    const float bm = fminf(fminf(fabsf(b1.x), fabsf(b1.y)), fminf(fabsf(b2.x), fabsf(b2.y)));
+                    any |= bm <= band[r].w;
+                    vA[r] = A;
+                    v2[r] = m2;
+                    v3[r] = m3;
+                    vj[r] = jd;
+                }
+                if (any) {
+                    const int jg = cur * kTJ + j;
+#pragma unroll
+                    for (int r = 0; r < kRT; ++r) {
+                        const float lo = band[r].lo, hi = band[r].hi;
+                        uint32_t f = ((vA[r] >= lo && vA[r] <= hi) ? 1u : 0u) |
+                                     ((v2[r] >= lo && v2[r] <= hi) ? 2u : 0u) |
+                                     ((v3[r] >= lo && v3[r] <= hi) ? 4u : 0u) |
+                                     ((vj[r] >= lo && vj[r] <= hi) ? 8u : 0u);
+                        f &= fmask;
+                        if (f) {
+                            const int idx = wrow + r * 32 + lane;
+                            if (nev[r] < kCap)
+                                ev[(ci.row0 + idx) * kCap + nev[r]] = (uint32_t)jg | (f << 28);
+                            ++nev[r];
+                        }
                     }
                 }
             }
         }
         __syncthreads();
-        if (threadIdx.x == 0 && t + 2 < ntile) ring_issue(ring, st, cp + (int64_t)(t + 2) * kTJ * DP);
+        if (warp == 0) {
+            const int st = next_stage<DP>(tv, spos, box128, stage0, wbox, wbound, c0, c1, false, prune);
+            if (lane == 0) {
+                sid[b] = st;
+                if (st >= 0) ring_issue(ring, b, cp + (int64_t)st * kTJ * DP);
+            }
+        }
+        __syncthreads();
     }
+    if (lane == 0 && wvalid) atomicAdd(work, (unsigned long long)nsub);
 #pragma unroll
     for (int r = 0; r < kRT; ++r) {
-        const int idx = tr.r0 + r * kNT + threadIdx.x;
+        const int idx = wrow + r * 32 + lane;
         if (idx >= ci.n) continue;
         const uint32_t self = band[r].lo > 0.0f ? 1u : 0u;  // the self pair counted as inside
         const int64_t row = ci.row0 + idx;
-        cnt_out[row] = (int32_t)(c0[r] - self);
-        cnt_out[total_rows + row] = (int32_t)(c1[r] - self);
-        cnt_out[2 * total_rows + row] = (int32_t)(c2[r] - self);
+        cnt_out[row] = (int32_t)(cA[r] - self);
+        cnt_out[ws_rows + row] = (int32_t)(c2[r] - self);
+        cnt_out[2 * ws_rows + row] = (int32_t)(c3[r] - self);
         ev_n[row] = nev[r];
     }
 }
 
 // ---------------------------------------------------------------------------
-// resolve: fp64 certification of band events
+// resolve: fp64 certification of band events (sorted positions -> rows via perm)
 // ---------------------------------------------------------------------------
 struct TeLayout {
     int dy;
@@ -428,20 +731,21 @@ __device__ __forceinline__ void te_dist64(const double *ref, const double *q, in
 
 __global__ void __launch_bounds__(kNT) resolve_kernel(
     const double *__restrict__ pts64, int dim, const ChunkInfo *__restrict__ info,
-    const TileRef *__restrict__ tiles, int k, TeLayout lay, const int32_t *__restrict__ L_in,
-    const int32_t *__restrict__ cnt_in, const uint32_t *__restrict__ ev,
-    const int32_t *__restrict__ ev_n, int64_t ws_rows, int64_t total_rows,
-    double *__restrict__ out_eps, int32_t *__restrict__ out_counts, int64_t *__restrict__ ovf_list,
-    int32_t *__restrict__ ovf_n) {
+    const TileRef *__restrict__ tiles, int k, TeLayout lay, const int32_t *__restrict__ perm,
+    const int32_t *__restrict__ L_in, const int32_t *__restrict__ cnt_in,
+    const uint32_t *__restrict__ ev, const int32_t *__restrict__ ev_n, int64_t ws_rows,
+    int64_t total_rows, double *__restrict__ out_eps, int32_t *__restrict__ out_counts,
+    int64_t *__restrict__ ovf_list, int32_t *__restrict__ ovf_n) {
     const TileRef tr = tiles[blockIdx.x];
     const ChunkInfo ci = info[tr.chunk];
     for (int r = 0; r < kRT; ++r) {
-        const int idx = tr.r0 + r * kNT + threadIdx.x;
-        if (idx >= ci.n) continue;
-        const int64_t row = ci.row0 + idx;
-        const int ne = ci.ok32 ? ev_n[row] : kCap + 1;
-        const int need = ci.ok32 ? k - L_in[row] : 0;
-        bool fallback = ne > kCap || need < 1;
+        const int s = tr.r0 + r * kNT + threadIdx.x;  // sorted position
+        if (s >= ci.n) continue;
+        const int64_t srow = ci.row0 + s;
+        const int64_t row = ci.ok32 ? ci.row0 + perm[srow] : srow;
+        const int ne = ci.ok32 ? ev_n[srow] : kCap + 1;
+        const int need = ci.ok32 ? k - L_in[srow] : 0;
+        bool fallback = !ci.ok32 || ne > kCap || need < 1;
         double eps = 0.0;
         int extra[3] = {0, 0, 0};
         if (!fallback) {
@@ -451,30 +755,29 @@ __global__ void __launch_bounds__(kNT) resolve_kernel(
             double dj[kCap];
             int nj = 0;
             for (int e = 0; e < ne; ++e) {
-                const uint32_t w = ev[row * kCap + e];
+                const uint32_t w = ev[srow * kCap + e];
                 const int j = (int)(w & 0x0FFFFFFFu);
-                if (j == idx || !(w >> 31)) continue;
+                if (j == s || !(w >> 31)) continue;
                 double A, m2, m3, jd;
-                te_dist64(ref, pts64 + (ci.row0 + j) * dim, dim, lay.dy, A, m2, m3, jd);
-                double x = jd;
+                te_dist64(ref, pts64 + (ci.row0 + perm[ci.row0 + j]) * dim, dim, lay.dy, A, m2, m3, jd);
                 int p = nj++;
-                while (p > 0 && dj[p - 1] > x) {
+                while (p > 0 && dj[p - 1] > jd) {
                     dj[p] = dj[p - 1];
                     --p;
                 }
-                dj[p] = x;
+                dj[p] = jd;
             }
             if (need > nj) {
                 fallback = true;
             } else {
                 eps = dj[need - 1];
                 for (int e = 0; e < ne; ++e) {
-                    const uint32_t w = ev[row * kCap + e];
+                    const uint32_t w = ev[srow * kCap + e];
                     const int j = (int)(w & 0x0FFFFFFFu);
                     const uint32_t f = (w >> 28) & 7u;
-                    if (j == idx || !f) continue;
+                    if (j == s || !f) continue;
                     double A, m2, m3, jd;
-                    te_dist64(ref, pts64 + (ci.row0 + j) * dim, dim, lay.dy, A, m2, m3, jd);
+                    te_dist64(ref, pts64 + (ci.row0 + perm[ci.row0 + j]) * dim, dim, lay.dy, A, m2, m3, jd);
                     extra[0] += (f & 1u) && (A < eps);
                     extra[1] += (f & 2u) && (m2 < eps);
                     extra[2] += (f & 4u) && (m3 < eps);
@@ -488,8 +791,8 @@ __global__ void __launch_bounds__(kNT) resolve_kernel(
         }
         out_eps[row] = eps;
         for (int o = 0; o < lay.nout; ++o) {
-            const int s = lay.slot[o];
-            out_counts[o * total_rows + row] = cnt_in[s * ws_rows + row] + extra[s];
+            const int sl = lay.slot[o];
+            out_counts[o * total_rows + row] = cnt_in[sl * ws_rows + srow] + extra[sl];
         }
     }
 }
@@ -589,9 +892,11 @@ __global__ void __launch_bounds__(kExactWarps * 32) exact_kernel(
 // ---------------------------------------------------------------------------
 // host side: kernel tables and dispatch
 // ---------------------------------------------------------------------------
-using KnnFn = void (*)(const float *, const ChunkInfo *, const TileRef *, int, float *, int32_t *);
-using CountFn = void (*)(const float *, const ChunkInfo *, const TileRef *, const float *, int64_t,
-                         int32_t *, uint32_t *, int32_t *, uint32_t);
+using KnnFn = void (*)(const float *, const float *, const float *, const ChunkInfo *,
+                       const TileRef *, int, int, float *, int32_t *, unsigned long long *);
+using CountFn = void (*)(const float *, const float *, const float *, const ChunkInfo *,
+                         const TileRef *, const float *, int64_t, FilterCols, int, int32_t *,
+                         uint32_t *, int32_t *, uint32_t, unsigned long long *);
 
 template <int D>
 static KnnFn knn_for_slots(int slots) {
@@ -636,9 +941,11 @@ struct Plan {
     bool fast = false;
     int dy = 0, dx = 0, slots = 0, dp = 0;
     TeLayout lay{};
+    FilterCols fc{};
     int64_t total_rows = 0;
     int64_t total_prows = 0;
     int n_tiles = 0;
+    int max_npad = 0;
 };
 
 // Map the requested marginals onto the TE layout [y | y-past(dy) | x-past(dx)].
@@ -665,6 +972,26 @@ static bool match_te_layout(int dim, const uint32_t *masks, int n_marg, int &dy_
     return false;
 }
 
+// Filter columns: the intersection of every requested marginal with the
+// joint, as a contiguous range (the TE marginals are ranges sharing y-past).
+static FilterCols filter_cols(int dim, int dy, const TeLayout &lay) {
+    int lo = 0, hi = dim;
+    for (int o = 0; o < lay.nout; ++o) {
+        switch (lay.slot[o]) {
+            case 0: lo = std::max(lo, 1); hi = std::min(hi, dy + 1); break;
+            case 1: hi = std::min(hi, dy + 1); break;
+            default: lo = std::max(lo, 1); break;
+        }
+    }
+    FilterCols fc{};
+    fc.f0 = lo;
+    fc.nf = std::max(0, hi - lo);
+    fc.bits = fc.nf > 0 ? std::min(10, 30 / fc.nf) : 0;
+    if (fc.nf > 0 && fc.bits == 0) fc.bits = 1;  // nf > 30: one bit per column
+    if (fc.nf * fc.bits > 32) fc.nf = 32 / fc.bits;  // Morton over a prefix
+    return fc;
+}
+
 static int exact_slots(int k) {
     if (k <= 4) return 4;
     if (k <= 8) return 8;
@@ -681,6 +1008,7 @@ static Plan make_plan(const ente_chunk *chunks, int n_chunks, int dim, const uin
         p.total_rows = std::max(p.total_rows, chunks[c].row0 + chunks[c].n);
         const int npad = round_up(chunks[c].n, kTJ);
         p.total_prows += npad;
+        p.max_npad = std::max(p.max_npad, npad);
         p.n_tiles += (chunks[c].n + kRefTile - 1) / kRefTile;
     }
     int dy = 0;
@@ -692,14 +1020,21 @@ static Plan make_plan(const ente_chunk *chunks, int n_chunks, int dim, const uin
         p.slots = k + 1;
         p.dp = (dim + 3) & ~3;
         p.lay = lay;
+        p.fc = filter_cols(dim, dy, lay);
     }
     return p;
 }
 
 struct SearchWs {
     ChunkInfo *info;
+    ColStats *stats;
     TileRef *tiles;
     float *pts32;
+    float *box32;
+    float *box128;
+    uint32_t *ka, *kb;
+    int32_t *va, *vb;
+    int32_t *perm;
     float *t32;
     int32_t *L;
     int32_t *cnt3;
@@ -707,15 +1042,25 @@ struct SearchWs {
     int32_t *ev_n;
     int64_t *ovf;
     int32_t *ovf_n;
+    unsigned long long *work;  // [0] knn sub-tiles evaluated, [1] count sub-tiles
 };
 
 static SearchWs layout_ws(Arena &a, const Plan &p, int n_chunks) {
     SearchWs w{};
     w.info = a.take<ChunkInfo>(n_chunks);
     w.ovf_n = a.take<int32_t>(1);
+    w.work = a.take<unsigned long long>(2);
     if (p.fast) {
+        w.stats = a.take<ColStats>(n_chunks);
         w.tiles = a.take<TileRef>(p.n_tiles);
         w.pts32 = a.take<float>((size_t)p.total_prows * p.dp);
+        w.box32 = a.take<float>((size_t)(p.total_prows / kSub) * 2 * p.dp);
+        w.box128 = a.take<float>((size_t)(p.total_prows / kTJ) * 2 * p.dp);
+        w.ka = a.take<uint32_t>(p.total_rows);
+        w.kb = a.take<uint32_t>(p.total_rows);
+        w.va = a.take<int32_t>(p.total_rows);
+        w.vb = a.take<int32_t>(p.total_rows);
+        w.perm = a.take<int32_t>(p.total_rows);
         w.t32 = a.take<float>(p.total_rows);
         w.L = a.take<int32_t>(p.total_rows);
         w.cnt3 = a.take<int32_t>((size_t)3 * p.total_rows);
@@ -745,9 +1090,10 @@ static void launch_exact(cudaStream_t st, const double *pts64, int dim, const Ch
                          const double *radii = nullptr) {
     int64_t blocks = list ? (int64_t)num_sms() * 8 : (dense_n + kExactWarps - 1) / kExactWarps;
     blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)num_sms() * 64));
-    exact_kernel<S><<<(unsigned)blocks, kExactWarps * 32, 0, st>>>(
-        pts64, dim, info, n_chunks, status, list, list_n, dense_n, k, masks, total_rows, radii,
-        out_eps, out_counts);
+    ENTE_LAUNCH("exact", st,
+                exact_kernel<S><<<(unsigned)blocks, kExactWarps * 32, 0, st>>>(
+                    pts64, dim, info, n_chunks, status, list, list_n, dense_n, k, masks,
+                    total_rows, radii, out_eps, out_counts));
 }
 
 static void dispatch_exact(int k, cudaStream_t st, const double *pts64, int dim,
@@ -820,6 +1166,18 @@ extern "C" size_t ente_search_workspace_size(const ente_chunk *chunks, int n_chu
     return a.used + 256;
 }
 
+static int g_prune = -1;  // ENTE_PRUNE=0 disables box pruning (measurement only)
+
+static int prune_enabled() {
+    if (g_prune < 0) {
+        const char *e = getenv("ENTE_PRUNE");
+        g_prune = (e && e[0] == '0') ? 0 : 1;
+    }
+    return g_prune;
+}
+
+static unsigned long long g_work[2] = {0, 0};
+
 extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
                            const ente_chunk *chunks, int n_chunks, const uint32_t *marg_masks,
                            int n_marg, int k, double *out_eps, int32_t *out_counts,
@@ -864,35 +1222,76 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
     ENTE_CUDA(cudaMemcpyAsync(status, hstatus.data(), sizeof(int32_t) * n_chunks,
                               cudaMemcpyHostToDevice, st));
     ENTE_CUDA(cudaMemsetAsync(w.ovf_n, 0, sizeof(int32_t), st));
-    prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, w.pts32, p.dp, status, p.fast ? 1 : 0);
-    ENTE_CUDA(cudaGetLastError());
     Masks masks{};
     masks.n = n_marg;
     for (int m = 0; m < n_marg; ++m) masks.m[m] = marg_masks[m];
     if (p.fast && !htiles.empty()) {
+        const int prune = prune_enabled();
+        ENTE_CUDA(cudaMemsetAsync(w.work, 0, 2 * sizeof(unsigned long long), st));
+        ENTE_LAUNCH("prep", st,
+                    prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, w.stats, status, 1));
+        ENTE_CUDA(cudaGetLastError());
+        FilterCols sfc = p.fc;
+        if (!prune) sfc.nf = 0;  // identity order
+        ENTE_LAUNCH("sort", st,
+                    sort_kernel<<<n_chunks, kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats, sfc,
+                                                                   w.ka, w.kb, w.va, w.vb, w.perm));
+        ENTE_CUDA(cudaGetLastError());
+        dim3 ggrid((unsigned)(p.max_npad / kTJ), (unsigned)std::min(n_chunks, 65535));
+        ENTE_LAUNCH("gather", st,
+                    gather_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.stats,
+                                                         w.perm, p.dp, w.pts32, w.box32,
+                                                         w.box128));
+        ENTE_CUDA(cudaGetLastError());
         ENTE_CUDA(cudaMemcpyAsync(w.tiles, htiles.data(), sizeof(TileRef) * htiles.size(),
                                   cudaMemcpyHostToDevice, st));
         const unsigned nt = (unsigned)htiles.size();
-        knn_table(dim, p.slots)<<<nt, kNT, 0, st>>>(w.pts32, w.info, w.tiles, k, w.t32, w.L);
+        ENTE_LAUNCH("knn_pass", st,
+                    knn_table(dim, p.slots)<<<nt, kNT, 0, st>>>(w.pts32, w.box32, w.box128, w.info,
+                                                               w.tiles, k, prune, w.t32, w.L,
+                                                               w.work));
         ENTE_CUDA(cudaGetLastError());
         uint32_t fmask = 8u;
         for (int o = 0; o < p.lay.nout; ++o) fmask |= 1u << p.lay.slot[o];
-        count_table(p.dy, p.dx)<<<nt, kNT, 0, st>>>(w.pts32, w.info, w.tiles, w.t32, ws_rows,
-                                                    w.cnt3, w.ev, w.ev_n, fmask);
+        ENTE_LAUNCH("count_pass", st,
+                    count_table(p.dy, p.dx)<<<nt, kNT, 0, st>>>(w.pts32, w.box32, w.box128, w.info,
+                                                                w.tiles, w.t32, ws_rows, p.fc,
+                                                                prune, w.cnt3, w.ev, w.ev_n, fmask,
+                                                                w.work + 1));
         ENTE_CUDA(cudaGetLastError());
-        resolve_kernel<<<nt, kNT, 0, st>>>(pts64, dim, w.info, w.tiles, k, p.lay, w.L, w.cnt3,
-                                           w.ev, w.ev_n, ws_rows, total_rows, out_eps, out_counts, w.ovf,
-                                           w.ovf_n);
+        ENTE_LAUNCH("resolve", st,
+                    resolve_kernel<<<nt, kNT, 0, st>>>(pts64, dim, w.info, w.tiles, k, p.lay,
+                                                       w.perm, w.L, w.cnt3, w.ev, w.ev_n, ws_rows,
+                                                       total_rows, out_eps, out_counts, w.ovf,
+                                                       w.ovf_n));
         ENTE_CUDA(cudaGetLastError());
         dispatch_exact(k, st, pts64, dim, w.info, n_chunks, status, w.ovf, w.ovf_n, 0, masks,
                        total_rows, out_eps, out_counts);
         ENTE_CUDA(cudaGetLastError());
+        if (ente_profile_enabled()) {
+            unsigned long long hw[2];
+            ENTE_CUDA(cudaMemcpyAsync(hw, w.work, sizeof(hw), cudaMemcpyDeviceToHost, st));
+            ENTE_CUDA(cudaStreamSynchronize(st));
+            g_work[0] += hw[0];
+            g_work[1] += hw[1];
+        }
     } else if (!p.fast) {
+        ENTE_LAUNCH("prep", st,
+                    prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, nullptr, status, 0));
+        ENTE_CUDA(cudaGetLastError());
         dispatch_exact(k, st, pts64, dim, w.info, n_chunks, status, nullptr, nullptr, total_rows,
                        masks, total_rows, out_eps, out_counts);
         ENTE_CUDA(cudaGetLastError());
     }
     return ENTE_OK;
+}
+
+// Evaluated 32-candidate x 128-reference sub-tiles of the two sweeps since the
+// last call (recorded while profiling is on): the pruned work actually done.
+extern "C" void ente_search_work(unsigned long long *knn_subtiles, unsigned long long *count_subtiles) {
+    *knn_subtiles = g_work[0];
+    *count_subtiles = g_work[1];
+    g_work[0] = g_work[1] = 0;
 }
 
 extern "C" size_t ente_radius_counts_workspace_size(int n_chunks) {

@@ -11,11 +11,11 @@
 #include <vector>
 
 #include "common.cuh"
+#include "profile.cuh"
+#include "radix.cuh"
 
 namespace ente {
 
-constexpr int kRedThreads = 256;
-constexpr int kRedWarps = kRedThreads / 32;
 
 __device__ __forceinline__ uint64_t f64_key(double v) {
     const uint64_t b = (uint64_t)__double_as_longlong(v);
@@ -58,12 +58,11 @@ struct RedChunk {
     int32_t pad_;
 };
 
-__global__ void __launch_bounds__(kRedThreads) te_reduce_kernel(
+__global__ void __launch_bounds__(kSortThreads) te_reduce_kernel(
     const int32_t *__restrict__ counts, int64_t total_rows, const RedChunk *__restrict__ chunks,
     const double *__restrict__ psi, int64_t table_len, double psi_k, uint64_t *__restrict__ ka,
     uint64_t *__restrict__ kb, double *__restrict__ out_te) {
-    __shared__ int hist[256];
-    __shared__ int wcnt[kRedWarps][256];
+    __shared__ SortSmem sm;
     __shared__ int bad;
     const RedChunk ch = chunks[blockIdx.x];
     const int n = ch.n;
@@ -71,7 +70,7 @@ __global__ void __launch_bounds__(kRedThreads) te_reduce_kernel(
     uint64_t *dst = kb + ch.row0;
     if (threadIdx.x == 0) bad = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += kRedThreads) {
+    for (int i = threadIdx.x; i < n; i += kSortThreads) {
         const int64_t row = ch.row0 + i;
         const int a = counts[row], b = counts[total_rows + row], c = counts[2 * total_rows + row];
         double v = 0.0;
@@ -84,58 +83,9 @@ __global__ void __launch_bounds__(kRedThreads) te_reduce_kernel(
         if (threadIdx.x == 0) out_te[blockIdx.x] = __longlong_as_double(0x7FF8000000000000ll);
         return;
     }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    for (int shift = 0; shift < 64; shift += 8) {
-        hist[threadIdx.x] = 0;
-        __syncthreads();
-        for (int i = threadIdx.x; i < n; i += kRedThreads) atomicAdd(&hist[(src[i] >> shift) & 255], 1);
-        __syncthreads();
-        bool single = false;
-        for (int d = 0; d < 256; ++d) single |= hist[d] == n;
-        __syncthreads();
-        if (single) continue;  // every key shares this digit: the pass is the identity
-        if (threadIdx.x == 0) {
-            int run = 0;
-            for (int d = 0; d < 256; ++d) {
-                const int h = hist[d];
-                hist[d] = run;
-                run += h;
-            }
-        }
-        __syncthreads();
-        // stable scatter, one 256-key tile at a time in input order
-        for (int base = 0; base < n; base += kRedThreads) {
-            const int i = base + threadIdx.x;
-            const bool valid = i < n;
-            const uint64_t key = valid ? src[i] : 0ull;
-            const int dig = valid ? (int)((key >> shift) & 255) : 256 + warp;
-#pragma unroll
-            for (int w = 0; w < kRedWarps; ++w) wcnt[w][threadIdx.x] = 0;
-            __syncthreads();
-            const unsigned peers = __match_any_sync(0xffffffffu, dig);
-            const int rank = __popc(peers & lt_mask);
-            if (valid && rank == 0) wcnt[warp][dig] = __popc(peers);
-            __syncthreads();
-            if (valid) {
-                int pre = 0;
-                for (int w = 0; w < warp; ++w) pre += wcnt[w][dig];
-                dst[hist[dig] + pre + rank] = key;
-            }
-            __syncthreads();
-            int add = 0;
-#pragma unroll
-            for (int w = 0; w < kRedWarps; ++w) add += wcnt[w][threadIdx.x];
-            hist[threadIdx.x] += add;
-            __syncthreads();
-        }
-        uint64_t *t = src;
-        src = dst;
-        dst = t;
-        __syncthreads();
-    }
+    const int parity = cta_radix_sort<uint64_t, int>(src, dst, nullptr, nullptr, n, 64, sm);
     if (threadIdx.x == 0) {
-        const double sum = pairwise(src, n);
+        const double sum = pairwise(parity ? dst : src, n);
         out_te[blockIdx.x] = __dadd_rn(psi_k, __ddiv_rn(sum, (double)n));
     }
 }
@@ -184,8 +134,10 @@ extern "C" int ente_te_reduce(const int32_t *counts, int64_t total_rows, const e
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ENTE_CUDA(cudaMemcpyAsync(dch, h.data(), sizeof(RedChunk) * n_chunks, cudaMemcpyHostToDevice, st));
-    te_reduce_kernel<<<n_chunks, kRedThreads, 0, st>>>(counts, total_rows, dch, psi_table, table_len,
-                                                      psi_k, ka, kb, out_te);
+    ENTE_LAUNCH("te_reduce", st,
+                te_reduce_kernel<<<n_chunks, kSortThreads, 0, st>>>(counts, total_rows, dch,
+                                                                  psi_table, table_len, psi_k, ka,
+                                                                  kb, out_te));
     ENTE_CUDA(cudaGetLastError());
     return ENTE_OK;
 }
