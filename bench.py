@@ -76,13 +76,18 @@ def items_of(wl, s):
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.window = None
+
+    def mark(self, t0, t1):
+        """Restrict the summary to samples taken in [t0, t1] (time.time())."""
+        self.window = (t0, t1)
 
     def __enter__(self):
         try:
@@ -108,16 +113,20 @@ class ClockSampler:
     def summary(self):
         if self.proc is None or not getattr(self, "lines", None):
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        import datetime
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                if self.window and not (self.window[0] - 0.25 <= ts <= self.window[1] + 0.25):
+                    continue
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
             except (ValueError, IndexError):
                 continue
-            for nm, v in zip(names, parts[3:7]):
+            for nm, v in zip(names, parts[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
@@ -219,13 +228,16 @@ def run_ours(args):
             dist.barrier()
             torch.cuda.synchronize()
 
+    clk = ClockSampler(local).__enter__()  # nvidia-smi start-up stays outside the timed region
     for _ in range(args.warmup):
         step()
     barrier()
+    nat.search_work()  # reset the evaluated-sub-tile counters
     launches0 = nat.launch_count()
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk, nat.KernelProfile():
+    with nat.KernelProfile():
+        t_abs = time.time()
         start.record()
         t_wall = time.perf_counter()
         for _ in range(args.steps):
@@ -233,8 +245,11 @@ def run_ours(args):
         stop.record()
         barrier()
         t_wall = time.perf_counter() - t_wall
+        clk.mark(t_abs, time.time())
         prof = nat.KernelProfile.read()
     launches = nat.launch_count() - launches0
+    knn_sub, cnt_sub = nat.search_work()
+    clk.__exit__(None, None, None)
     ms = start.elapsed_time(stop) / args.steps
     if dist is not None:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -261,6 +276,11 @@ def run_ours(args):
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(dom)
     total_ms = sum(v["ms"] for v in prof.values())
+    # pruned work actually evaluated: sub-tiles of 32 candidates x 128 references
+    sub_pce = 32 * 128 * dim
+    evaluated = {k: n * sub_pce / max(1, prof.get(k, {}).get("launches", 1))
+                 for k, n in (("knn_pass", knn_sub), ("count_pass", cnt_sub))}
+    ev_rate = 2.0 * evaluated[dom] / (per_launch_ms * 1e-3) / 1e12
     roofline = {"bound": "fp32", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
                 "frac": achieved / nominal, "traffic": traffic, "kernel": dom,
                 "peak_kind": f"nominal: {props.multi_processor_count} SMs x 128 lanes x 2 ops x "
@@ -271,6 +291,10 @@ def run_ours(args):
                 "kernel_share_of_step": prof[dom]["ms"] / total_ms if total_ms else None,
                 "kernels_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
                 "pce_per_launch": pce_pass,
+                "evaluated_pce_per_launch": evaluated,
+                "evaluated_fraction": {k: v / pce_pass for k, v in evaluated.items()},
+                "evaluated_tflops": ev_rate,
+                "evaluated_frac": ev_rate / nominal,
                 "work_definition": "ordered pairs x columns (n(n-1)D per pass, 2 passes; "
                                    "SURVEY 8d), 2 FP32 ops per pair-coordinate"}
 

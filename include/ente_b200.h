@@ -181,8 +181,8 @@ void ente_profile_reset(void);
 int ente_profile_read(char *names, size_t names_len, int64_t *launches, double *ms,
                       int max_kernels);
 int ente_microbench_pce(int iters, int blocks, double *pce_per_s, void *stream);
-/* sub-tiles (32 candidates x 128 references) the two sweeps evaluated since
- * the last call, counted while profiling is on (pruning leaves the rest) */
+/* sub-tiles (32 candidates x 128 references) the two sweeps evaluated on the
+ * current device since the last call (pruning skips the rest); synchronises */
 void ente_search_work(unsigned long long *knn_subtiles, unsigned long long *count_subtiles);
 
 #ifdef __cplusplus

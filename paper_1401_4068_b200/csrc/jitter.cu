@@ -94,15 +94,17 @@ constexpr int kJitPerThread = 64;
 
 __global__ void __launch_bounds__(256) jitter_apply_kernel(double *__restrict__ pts, int dim,
                                                            const JitChunk *__restrict__ ch,
-                                                           const double *__restrict__ half_width) {
-    const JitChunk c = ch[blockIdx.y];
+                                                           const double *__restrict__ half_width,
+                                                           int n_chunks) {
+    for (int ci = blockIdx.y; ci < n_chunks; ci += gridDim.y) {  // grid.y <= 65535
+    const JitChunk c = ch[ci];
     const int64_t total = (int64_t)c.n * dim;
     const int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kJitPerThread;
-    if (e0 >= total) return;
+    if (e0 >= total) continue;
     const int64_t e1 = e0 + kJitPerThread < total ? e0 + kJitPerThread : total;
     U128 s = pcg_advance(c.state, c.inc, (uint64_t)e0);
     double *p = pts + c.row0 * dim;
-    const double *hw = half_width + (int64_t)blockIdx.y * kMaxDim;
+    const double *hw = half_width + (int64_t)ci * kMaxDim;
     int col = (int)(e0 % dim);
     for (int64_t e = e0; e < e1; ++e) {
         s = add128(mul128(s, kPcgMult), c.inc);
@@ -111,6 +113,7 @@ __global__ void __launch_bounds__(256) jitter_apply_kernel(double *__restrict__ 
         const double u = __dadd_rn(-1.0, 2.0 * u01);
         p[e] = __dadd_rn(p[e], __dmul_rn(u, hw[col]));
         if (++col == dim) col = 0;
+    }
     }
 }
 
@@ -229,9 +232,9 @@ extern "C" int ente_jitter(double *pts64, int dim, const ente_chunk *chunks, int
         ENTE_CUDA(cudaGetLastError());
         const int64_t per_block = 256LL * kJitPerThread;
         const int64_t gx = ((int64_t)max_n * dim + per_block - 1) / per_block;
-        dim3 grid((unsigned)gx, (unsigned)n_chunks);
+        dim3 grid((unsigned)gx, (unsigned)(n_chunks < 65535 ? n_chunks : 65535));
         ENTE_LAUNCH("jitter_apply", st,
-                    jitter_apply_kernel<<<grid, 256, 0, st>>>(pts64, dim, w.ch, w.hw));
+                    jitter_apply_kernel<<<grid, 256, 0, st>>>(pts64, dim, w.ch, w.hw, n_chunks));
         ENTE_CUDA(cudaGetLastError());
     }
     ENTE_LAUNCH("check", st, check_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.ch, status));

@@ -24,12 +24,12 @@ struct PackItem {
 
 __global__ void __launch_bounds__(256) pack_te_kernel(
     const double *__restrict__ x, const double *__restrict__ y, int reps, int n_samples, int dx,
-    int tau_x, int dy, int tau_y, int t_lo, int w, const PackItem *__restrict__ items,
+    int tau_x, int dy, int tau_y, int t_lo, int w, const PackItem *__restrict__ items, int n_items,
     const int32_t *__restrict__ perms, double *__restrict__ out) {
-    const int item = blockIdx.y;
     const int64_t rows = (int64_t)reps * w;
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= rows) return;
+    for (int item = blockIdx.y; item < n_items; item += gridDim.y) {  // grid.y <= 65535
     const PackItem it = items[item];
     const int r = (int)(row / w);
     const int tp = t_lo + (int)(row - (int64_t)r * w);  // 1-based t'
@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(256) pack_te_kernel(
     o[0] = yr[tp - 1];
     for (int j = 0; j < dy; ++j) o[1 + j] = yr[tp - 2 - j * tau_y];
     for (int j = 0; j < dx; ++j) o[1 + dy + j] = xr[tp - 1 - it.u - j * tau_x];
+    }
 }
 
 }  // namespace ente
@@ -76,10 +77,10 @@ extern "C" int ente_pack_te(const double *x, const double *y, int reps, int n_sa
     ENTE_CUDA(cudaMallocAsync(&ditems, sizeof(PackItem) * n_items, st));
     ENTE_CUDA(cudaMemcpyAsync(ditems, items, sizeof(PackItem) * n_items, cudaMemcpyHostToDevice, st));
     const int64_t rows = (int64_t)reps * w;
-    dim3 grid((unsigned)((rows + 255) / 256), (unsigned)n_items);
+    dim3 grid((unsigned)((rows + 255) / 256), (unsigned)(n_items < 65535 ? n_items : 65535));
     ENTE_LAUNCH("pack_te", st,
                 pack_te_kernel<<<grid, 256, 0, st>>>(x, y, reps, n_samples, dx, tau_x, dy, tau_y,
-                                                     t_lo, w, ditems, perms, out));
+                                                     t_lo, w, ditems, n_items, perms, out));
     ENTE_CUDA(cudaGetLastError());
     ENTE_CUDA(cudaFreeAsync(ditems, st));
     return ENTE_OK;

@@ -1042,14 +1042,12 @@ struct SearchWs {
     int32_t *ev_n;
     int64_t *ovf;
     int32_t *ovf_n;
-    unsigned long long *work;  // [0] knn sub-tiles evaluated, [1] count sub-tiles
 };
 
 static SearchWs layout_ws(Arena &a, const Plan &p, int n_chunks) {
     SearchWs w{};
     w.info = a.take<ChunkInfo>(n_chunks);
     w.ovf_n = a.take<int32_t>(1);
-    w.work = a.take<unsigned long long>(2);
     if (p.fast) {
         w.stats = a.take<ColStats>(n_chunks);
         w.tiles = a.take<TileRef>(p.n_tiles);
@@ -1176,7 +1174,22 @@ static int prune_enabled() {
     return g_prune;
 }
 
-static unsigned long long g_work[2] = {0, 0};
+// Per-device running totals of evaluated sub-tiles ([0] knn, [1] count),
+// accumulated by the sweeps themselves (one atomic per warp, no host sync).
+static unsigned long long *g_dwork[64] = {nullptr};
+
+static unsigned long long *device_work() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!g_dwork[dev]) {
+        void *p = nullptr;
+        if (cudaMalloc(&p, 2 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+        cudaMemset(p, 0, 2 * sizeof(unsigned long long));
+        g_dwork[dev] = static_cast<unsigned long long *>(p);
+    }
+    return g_dwork[dev];
+}
 
 extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
                            const ente_chunk *chunks, int n_chunks, const uint32_t *marg_masks,
@@ -1227,7 +1240,11 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
     for (int m = 0; m < n_marg; ++m) masks.m[m] = marg_masks[m];
     if (p.fast && !htiles.empty()) {
         const int prune = prune_enabled();
-        ENTE_CUDA(cudaMemsetAsync(w.work, 0, 2 * sizeof(unsigned long long), st));
+        unsigned long long *work = device_work();
+        if (!work) {
+            set_error("ente_search: cannot allocate the work counters");
+            return ENTE_ERR_CUDA;
+        }
         ENTE_LAUNCH("prep", st,
                     prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, w.stats, status, 1));
         ENTE_CUDA(cudaGetLastError());
@@ -1249,7 +1266,7 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
         ENTE_LAUNCH("knn_pass", st,
                     knn_table(dim, p.slots)<<<nt, kNT, 0, st>>>(w.pts32, w.box32, w.box128, w.info,
                                                                w.tiles, k, prune, w.t32, w.L,
-                                                               w.work));
+                                                               work));
         ENTE_CUDA(cudaGetLastError());
         uint32_t fmask = 8u;
         for (int o = 0; o < p.lay.nout; ++o) fmask |= 1u << p.lay.slot[o];
@@ -1257,7 +1274,7 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
                     count_table(p.dy, p.dx)<<<nt, kNT, 0, st>>>(w.pts32, w.box32, w.box128, w.info,
                                                                 w.tiles, w.t32, ws_rows, p.fc,
                                                                 prune, w.cnt3, w.ev, w.ev_n, fmask,
-                                                                w.work + 1));
+                                                                work + 1));
         ENTE_CUDA(cudaGetLastError());
         ENTE_LAUNCH("resolve", st,
                     resolve_kernel<<<nt, kNT, 0, st>>>(pts64, dim, w.info, w.tiles, k, p.lay,
@@ -1268,13 +1285,6 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
         dispatch_exact(k, st, pts64, dim, w.info, n_chunks, status, w.ovf, w.ovf_n, 0, masks,
                        total_rows, out_eps, out_counts);
         ENTE_CUDA(cudaGetLastError());
-        if (ente_profile_enabled()) {
-            unsigned long long hw[2];
-            ENTE_CUDA(cudaMemcpyAsync(hw, w.work, sizeof(hw), cudaMemcpyDeviceToHost, st));
-            ENTE_CUDA(cudaStreamSynchronize(st));
-            g_work[0] += hw[0];
-            g_work[1] += hw[1];
-        }
     } else if (!p.fast) {
         ENTE_LAUNCH("prep", st,
                     prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, nullptr, status, 0));
@@ -1286,12 +1296,16 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
     return ENTE_OK;
 }
 
-// Evaluated 32-candidate x 128-reference sub-tiles of the two sweeps since the
-// last call (recorded while profiling is on): the pruned work actually done.
+// Evaluated 32-candidate x 128-reference sub-tiles of the two sweeps on the
+// current device since the last call (synchronises the device): the pruned
+// work actually done.
 extern "C" void ente_search_work(unsigned long long *knn_subtiles, unsigned long long *count_subtiles) {
-    *knn_subtiles = g_work[0];
-    *count_subtiles = g_work[1];
-    g_work[0] = g_work[1] = 0;
+    unsigned long long h[2] = {0, 0};
+    unsigned long long *d = device_work();
+    if (d && cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess)
+        cudaMemset(d, 0, sizeof(h));
+    *knn_subtiles = h[0];
+    *count_subtiles = h[1];
 }
 
 extern "C" size_t ente_radius_counts_workspace_size(int n_chunks) {

@@ -154,3 +154,41 @@ def test_batch_equals_singles():
         (s,) = batch_search([(c, margs)], 4)
         assert np.array_equal(s.kth_distance, b.kth_distance)
         assert all(np.array_equal(x, y) for x, y in zip(s.radius_counts, b.radius_counts))
+
+
+@pytest.mark.parametrize("subset", [(0,), (1,), (2,), (1, 2), (2, 0), ()])
+def test_marginal_subsets_choose_exact_filter(subset):
+    # every subset of the TE marginals selects its own pruning columns
+    rng = np.random.default_rng(len(subset) * 7 + sum(subset))
+    d_y, d_x = 3, 3
+    full = cases.te_margs(d_y, d_x)
+    margs = [full[s] for s in subset]
+    t = np.cumsum(rng.standard_normal((4000, 1)), axis=0) * 0.05
+    pts = np.concatenate([np.sin(t * (c + 1)) + 1e-3 * rng.standard_normal((4000, 1))
+                          for c in range(1 + d_y + d_x)], axis=1)
+    (r,) = batch_search([(Chunk(pts), margs)], 4)
+    e, c = oracle.search(pts, margs, 4)
+    assert np.array_equal(r.kth_distance, e)
+    for a, b in zip(r.radius_counts, c):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("kind", ["clustered", "lorenz_like", "round"])
+def test_pruned_sweep_large_chunks(kind):
+    # multi-stage traversal with heavy pruning: clustered / attractor-like data
+    rng = np.random.default_rng(11)
+    n = 9000
+    if kind == "clustered":
+        centres = rng.standard_normal((12, 7)) * 10
+        pts = centres[rng.integers(0, 12, n)] + 0.1 * rng.standard_normal((n, 7))
+    elif kind == "lorenz_like":
+        s = np.cumsum(rng.standard_normal(n + 10)) * 0.1
+        pts = np.stack([np.sin(s[i:i + n] * 0.7 + i) for i in range(7)], axis=1)
+    else:
+        pts = np.round(rng.standard_normal((n, 7)), 1)
+    margs = cases.te_margs(3, 3)
+    (r,) = batch_search([(Chunk(pts), margs)], 4)
+    e, c = oracle.search(pts, margs, 4)
+    assert np.array_equal(r.kth_distance, e)
+    for a, b in zip(r.radius_counts, c):
+        assert np.array_equal(a, b)
