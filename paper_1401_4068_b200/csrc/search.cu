@@ -42,9 +42,9 @@ namespace ente {
 // ---------------------------------------------------------------------------
 // prep: column statistics, error bound, finiteness
 // ---------------------------------------------------------------------------
-constexpr int kSub = 32;                    // rows per sub-tile box (one warp of candidates)
-constexpr int kSubPerStage = kTJ / kSub;    // sub-tiles per shared-memory stage
-constexpr int kWarps = kNT / 32;            // warps per sweep CTA; warp w owns 128 refs
+constexpr int kSub = 32;                    // candidate rows per sub-tile (one TMA copy)
+constexpr int kWarpRefs = 32 * kRT;         // references per sweep CTA (one warp)
+constexpr int kGate = 4;                    // gate columns in the Morton key and the boxes
 
 // per-chunk column statistics (fp64): mean, min, max of the raw values
 struct ColStats {
@@ -165,118 +165,104 @@ __global__ void __launch_bounds__(kSortThreads) sort_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// gather: sorted fp32 rows (centred) + bounding boxes per 32 and 128 rows
-// box layout: [lo[0..dp) | hi[0..dp)] per tile
+// gather: sorted fp32 rows (centred, D padded to DP) + per-32-row boxes over
+// the gate columns (fbox layout per sub-tile: lo[kGate] | hi[kGate]; unused
+// gate slots hold 0 so they add nothing to a box distance)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kTJ) gather_kernel(const double *__restrict__ pts64, int dim,
                                                      const ChunkInfo *__restrict__ info, int n_chunks,
                                                      const ColStats *__restrict__ stats,
                                                      const int32_t *__restrict__ perm, int dp,
-                                                     float *__restrict__ pts32,
-                                                     float *__restrict__ box32,
-                                                     float *__restrict__ box128) {
-    __shared__ float slo[kTJ / 32][kMaxDim], shi[kTJ / 32][kMaxDim];
+                                                     FilterCols fc, float *__restrict__ pts32,
+                                                     float *__restrict__ fbox) {
     for (int cidx = blockIdx.y; cidx < n_chunks; cidx += gridDim.y) {
-    const ChunkInfo ci = info[cidx];
-    const int stage = blockIdx.x;
-    if (!ci.ok32 || stage * kTJ >= ci.npad) continue;
-    const ColStats *cs = stats + cidx;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int s = stage * kTJ + threadIdx.x;
-    const bool valid = s < ci.n;
-    const int64_t orig = valid ? ci.row0 + perm[ci.row0 + s] : 0;
-    float *q = pts32 + (ci.prow0 + s) * dp;
-    const int64_t sub = ci.prow0 / kSub + stage * kSubPerStage + warp;
-    for (int col = 0; col < dp; ++col) {
-        float v = 0.0f;
-        if (col < dim)
-            v = valid ? __double2float_rn(__dsub_rn(pts64[orig * dim + col], cs->mean[col])) : INFINITY;
-        q[col] = v;
-        float lo = (valid && col < dim) ? v : INFINITY;
-        float hi = (valid && col < dim) ? v : -INFINITY;
+        const ChunkInfo ci = info[cidx];
+        const int stage = blockIdx.x;
+        if (!ci.ok32 || stage * kTJ >= ci.npad) continue;
+        const ColStats *cs = stats + cidx;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int s = stage * kTJ + threadIdx.x;
+        const bool valid = s < ci.n;
+        const int64_t orig = valid ? ci.row0 + perm[ci.row0 + s] : 0;
+        float *q = pts32 + (ci.prow0 + s) * dp;
+        const int64_t sub = ci.prow0 / kSub + stage * (kTJ / kSub) + warp;
+        for (int col = 0; col < dp; ++col) {
+            float v = 0.0f;
+            if (col < dim)
+                v = valid ? __double2float_rn(__dsub_rn(pts64[orig * dim + col], cs->mean[col]))
+                          : INFINITY;
+            q[col] = v;
+            const int g = col - fc.f0;
+            if (g >= 0 && g < kGate) {  // warp-uniform
+                float lo = 0.0f, hi = 0.0f;
+                if (g < fc.nf) {
+                    lo = valid ? v : INFINITY;
+                    hi = valid ? v : -INFINITY;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
-            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, off));
-        }
-        if (lane == 0) {
-            box32[sub * 2 * dp + col] = lo;
-            box32[sub * 2 * dp + dp + col] = hi;
-            if (col < kMaxDim) {
-                slo[warp][col] = lo;
-                shi[warp][col] = hi;
+                    for (int off = 16; off > 0; off >>= 1) {
+                        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+                        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+                    }
+                }
+                if (lane == 0) {
+                    fbox[sub * 2 * kGate + g] = lo;
+                    fbox[sub * 2 * kGate + kGate + g] = hi;
+                }
             }
         }
-    }
-    __syncthreads();
-    if (threadIdx.x < dp) {
-        const int col = threadIdx.x;
-        float lo = INFINITY, hi = -INFINITY;
-        for (int w = 0; w < kTJ / 32; ++w) {
-            lo = fminf(lo, slo[w][col]);
-            hi = fmaxf(hi, shi[w][col]);
-        }
-        const int64_t t = ci.prow0 / kTJ + stage;
-        box128[t * 2 * dp + col] = lo;
-        box128[t * 2 * dp + dp + col] = hi;
-    }
-    __syncthreads();
+        // gate slots beyond the columns (dim < f0 + kGate)
+        if (lane == 0)
+            for (int g = dim - fc.f0; g < kGate; ++g)
+                if (g >= 0) fbox[sub * 2 * kGate + g] = fbox[sub * 2 * kGate + kGate + g] = 0.0f;
     }
 }
 
 // ---------------------------------------------------------------------------
 // register-level helpers for the fp32 sweeps
+// TE layout columns: 0 = y_t, 1..DY = y-past, DY+1..D-1 = x-past
+// (embedding.py:50-60).  Coordinates are held as packed pairs (0,1), (2,3)...
+// so one FADD2 gives two differences.  Pairs [0, PG) cover columns 0..DY
+// (the gate: y-past plus y_t), pairs [PG, NP) the rest.
 // ---------------------------------------------------------------------------
-template <int D>
-struct Ref {
-    static constexpr int NP = (D + 1) / 2;
-    float2 nr[NP];  // negated coordinates, packed for FADD2
+template <int DY, int DX>
+struct Lay {
+    static constexpr int D = 1 + DY + DX;
+    static constexpr int DP = (D + 3) & ~3;
+    static constexpr int NP = (D + 1) / 2;     // coordinate pairs
+    static constexpr int PG = (DY + 2) / 2;    // gate pairs: columns 0 .. 2*PG-1 >= DY
+    static constexpr int NSLOT = DP <= 8 ? 8 : (DP <= 12 ? 6 : 4);  // ring slots per warp
 };
 
 template <int D>
-__device__ __forceinline__ void load_ref(Ref<D> &ref, const float *__restrict__ row, bool valid) {
+__device__ __forceinline__ void load_ref(float2 (&nr)[(D + 1) / 2], const float *__restrict__ row,
+                                         bool valid) {
 #pragma unroll
-    for (int p = 0; p < Ref<D>::NP; ++p) {
-        float a = valid ? row[2 * p] : 0.0f;
-        float b = (valid && 2 * p + 1 < D) ? row[2 * p + 1] : 0.0f;
-        ref.nr[p] = make_float2(-a, -b);
+    for (int p = 0; p < (D + 1) / 2; ++p) {
+        const float a = valid ? row[2 * p] : 0.0f;
+        const float b = (valid && 2 * p + 1 < D) ? row[2 * p + 1] : 0.0f;
+        nr[p] = make_float2(-a, -b);
     }
 }
 
-template <int D>
-struct Cand {
-    static constexpr int DP = (D + 3) & ~3;
-    float4 v[DP / 4];
-    __device__ __forceinline__ float2 pair(int p) const {
-        const float4 &q = v[p >> 1];
-        return (p & 1) ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
-    }
-    __device__ __forceinline__ float at(int c) const {
-        const float4 &q = v[c >> 2];
-        switch (c & 3) {
-            case 0: return q.x;
-            case 1: return q.y;
-            case 2: return q.z;
-            default: return q.w;
+// difference pairs [P0, P1) of ref (negated, packed) and candidate row (smem)
+template <int D, int P0, int P1>
+__device__ __forceinline__ void diff_pairs(const float2 (&nr)[(D + 1) / 2], const float2 *c,
+                                           float (&a)[2 * ((D + 1) / 2)]) {
+#pragma unroll
+    for (int p = P0; p < P1; ++p) {
+        if (2 * p + 1 < D) {
+            const float2 d = __fadd2_rn(nr[p], c[p]);
+            a[2 * p] = d.x;
+            a[2 * p + 1] = d.y;
+        } else {
+            a[2 * p] = nr[p].x + c[p].x;
         }
     }
-};
-
-// signed differences x_ref - x_cand (sign irrelevant: only |.| is used)
-template <int D>
-__device__ __forceinline__ void diffs(const Ref<D> &ref, const Cand<D> &c, float (&a)[D]) {
-#pragma unroll
-    for (int p = 0; p < D / 2; ++p) {
-        float2 d = __fadd2_rn(ref.nr[p], c.pair(p));
-        a[2 * p] = d.x;
-        a[2 * p + 1] = d.y;
-    }
-    if (D & 1) a[D - 1] = ref.nr[D / 2].x + c.at(D - 1);
 }
 
-// max |a[c]| for c in [LO, HI), folded into acc (3-input FMNMX chain)
-template <int LO, int HI, int D>
-__device__ __forceinline__ float maxabs(const float (&a)[D], float acc) {
+// max |a[c]| for c in [LO, HI) folded into acc (3-input FMNMX chain)
+template <int LO, int HI, int N>
+__device__ __forceinline__ float maxabs(const float (&a)[N], float acc) {
     int c = LO;
 #pragma unroll
     for (; c + 1 < HI; c += 2) acc = fmaxf(fmaxf(acc, fabsf(a[c])), fabsf(a[c + 1]));
@@ -284,11 +270,11 @@ __device__ __forceinline__ float maxabs(const float (&a)[D], float acc) {
     return acc;
 }
 
-template <int LO, int HI, int D>
-__device__ __forceinline__ float maxabs0(const float (&a)[D]) {
+template <int LO, int HI, int N>
+__device__ __forceinline__ float maxabs0(const float (&a)[N]) {
     if constexpr (HI - LO <= 0) return 0.0f;
     else if constexpr (HI - LO == 1) return fabsf(a[LO]);
-    else return maxabs<LO + 2, HI, D>(a, fmaxf(fabsf(a[LO]), fabsf(a[LO + 1])));
+    else return maxabs<LO + 2, HI, N>(a, fmaxf(fabsf(a[LO]), fabsf(a[LO + 1])));
 }
 
 // Keep the S smallest values, ascending (new[s] = median(old[s-1], old[s], d));
@@ -298,21 +284,6 @@ __device__ __forceinline__ void insert_sorted(float (&kd)[S], float d) {
 #pragma unroll
     for (int s = S - 1; s >= 1; --s) kd[s] = fmaxf(kd[s - 1], fminf(kd[s], d));
     kd[0] = fminf(kd[0], d);
-}
-
-// Shared-memory candidate ring fed by 1-D TMA bulk copies.
-template <int DP>
-struct Ring {
-    float buf[2][kTJ * DP];
-    uint64_t full[2];
-};
-
-template <int DP>
-__device__ __forceinline__ void ring_issue(Ring<DP> &ring, int stage, const float *src) {
-    constexpr uint32_t bytes = kTJ * DP * sizeof(float);
-    fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&ring.full[stage], bytes);
-    bulk_g2s(ring.buf[stage], src, bytes, &ring.full[stage]);
 }
 
 struct Band {
@@ -334,110 +305,129 @@ __device__ __forceinline__ Band make_band(float t32, double delta) {
     return b;
 }
 
-// ---------------------------------------------------------------------------
-// traversal: candidate stages visited home-first, then alternately below and
-// above (spatially nearest first in the Morton order, so kNN bounds shrink
-// early); warp 0 evaluates 32 positions at a time and picks the first stage
-// some warp still needs (its box distance below that warp's bound)
-// ---------------------------------------------------------------------------
-struct Trav {
-    int h0, nh, nst, npos;
-    __device__ void init(int r0, int n, int npad) {
-        h0 = r0 / kTJ;
-        nh = (min(r0 + kRefTile, n) - r0 + kTJ - 1) / kTJ;
-        nst = npad / kTJ;
-        npos = nh + 2 * max(h0, nst - h0 - nh);
-    }
-    __device__ int stage_at(int pos) const {
-        if (pos < nh) return h0 + pos;
-        const int p = pos - nh, k = (p >> 1) + 1;
-        const int s = (p & 1) ? h0 + nh - 1 + k : h0 - k;
-        return (s >= 0 && s < nst) ? s : -1;
-    }
-};
-
-// fp32 box distance over columns [c0, c1): a lower bound of every d32 between
-// the two boxes (fl is monotone: fl(x_j - x_i) >= fl(lo_j - hi_i))
-template <int DP>
-__device__ __forceinline__ float box_dist(const float *a, const float *b, int c0, int c1) {
-    float m = 0.0f;
-#pragma unroll
-    for (int c = 0; c < DP; ++c) {
-        if (c < c0 || c >= c1) continue;
-        m = fmaxf(m, fmaxf(b[c] - a[DP + c], a[c] - b[DP + c]));
-    }
-    return m;
-}
-
 __device__ __forceinline__ float warp_max_nonneg(float v) {
     return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(v, 0.0f))));
 }
 
-// Warp 0: next stage to load (or -1).  strict: process iff dist < bound (kNN);
-// otherwise iff dist <= bound (counts: the band is closed at hi).
-template <int DP>
-__device__ __forceinline__ int next_stage(const Trav &tv, int &spos, const float *box128,
-                                          int64_t stage0, const float (*wbox)[2 * DP],
-                                          const float *wbound, int c0, int c1, bool strict,
-                                          int prune) {
-    const int lane = threadIdx.x & 31;
-    while (spos < tv.npos) {
-        const int pos = spos + lane;
-        const int st = pos < tv.npos ? tv.stage_at(pos) : -1;
-        bool take = false;
-        if (st >= 0) {
-            if (!prune) {
-                take = true;
-            } else {
-                const float *bb = box128 + (stage0 + st) * 2 * DP;
-#pragma unroll
-                for (int w = 0; w < kWarps; ++w) {
-                    const float d = box_dist<DP>(wbox[w], bb, c0, c1);
-                    take |= strict ? (d < wbound[w]) : (d <= wbound[w]);
-                }
+// ---------------------------------------------------------------------------
+// Warp-private candidate stream.
+//
+// Each sweep CTA is ONE warp owning 128 consecutive sorted references (4 per
+// lane).  It walks the chunk's 32-row sub-tiles home-first, then alternately
+// below and above (nearest first in the Morton order, so kNN bounds shrink
+// early).  Sub-tile boxes are tested 32 positions at a time, one per lane,
+// with the next window's boxes prefetched into registers; needed sub-tiles
+// are streamed into a ring of NSLOT shared-memory slots by the TMA engine
+// (cp.async.bulk + mbarrier).  Warps never wait for each other.
+// ---------------------------------------------------------------------------
+struct Walker {
+    int h0, nh, nsub, npos;
+    int base;       // first position of the evaluated window (-32 before the first)
+    uint32_t mask;  // needed positions of that window not yet issued
+    int wst;        // per lane: sub-tile at position base + lane (-1: none)
+    float wd;       // per lane: its box distance
+    int nst;        // per lane: sub-tile at position base + 32 + lane (prefetched)
+    float4 nlo, nhi;
+    float4 blo, bhi;  // the warp's own box (gate columns), identical in all lanes
+
+    __device__ int sub_at(int pos) const {
+        if (pos < nh) return h0 + pos;
+        const int p = pos - nh, k = (p >> 1) + 1;
+        const int s = (p & 1) ? h0 + nh - 1 + k : h0 - k;
+        return (s >= 0 && s < nsub) ? s : -1;
+    }
+
+    __device__ void prefetch(const float4 *__restrict__ fb, int pos) {
+        nst = pos < npos ? sub_at(pos) : -1;
+        if (nst >= 0) {
+            nlo = __ldg(fb + 2 * nst);
+            nhi = __ldg(fb + 2 * nst + 1);
+        }
+    }
+
+    __device__ void init(const float4 *__restrict__ fb, int wrow, int n, int npad) {
+        h0 = wrow / kSub;
+        nh = (min(wrow + 32 * kRT, n) - wrow + kSub - 1) / kSub;
+        nsub = npad / kSub;
+        npos = nh + 2 * max(h0, nsub - h0 - nh);
+        base = -32;
+        mask = 0;
+        blo = __ldg(fb + 2 * h0);
+        bhi = __ldg(fb + 2 * h0 + 1);
+        for (int s = 1; s < nh; ++s) {
+            const float4 l = __ldg(fb + 2 * (h0 + s)), h = __ldg(fb + 2 * (h0 + s) + 1);
+            blo = make_float4(fminf(blo.x, l.x), fminf(blo.y, l.y), fminf(blo.z, l.z), fminf(blo.w, l.w));
+            bhi = make_float4(fmaxf(bhi.x, h.x), fmaxf(bhi.y, h.y), fmaxf(bhi.z, h.z), fmaxf(bhi.w, h.w));
+        }
+        prefetch(fb, (threadIdx.x & 31));
+    }
+
+    // fp32 box distance (a lower bound of every d32 between the two boxes:
+    // fl is monotone, fl(x_j - x_i) >= fl(lo_j - hi_i))
+    __device__ float dist(float4 lo, float4 hi) const {
+        const float a = fmaxf(fmaxf(lo.x - bhi.x, blo.x - hi.x), fmaxf(lo.y - bhi.y, blo.y - hi.y));
+        const float b = fmaxf(fmaxf(lo.z - bhi.z, blo.z - hi.z), fmaxf(lo.w - bhi.w, blo.w - hi.w));
+        return fmaxf(fmaxf(a, b), 0.0f);
+    }
+
+    // Next sub-tile whose box distance is below `bound` (strict) or not above
+    // it; returns -1 when the walk is over.
+    __device__ int next(const float4 *__restrict__ fb, float bound, bool strict, float &d_out) {
+        const int lane = threadIdx.x & 31;
+        for (;;) {
+            while (mask == 0) {
+                if (base + 32 >= npos) return -1;
+                base += 32;
+                wst = nst;
+                wd = wst >= 0 ? dist(nlo, nhi) : INFINITY;
+                mask = __ballot_sync(0xffffffffu, strict ? (wd < bound) : (wd <= bound));
+                prefetch(fb, base + 32 + lane);
+            }
+            const int b = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const float d = __shfl_sync(0xffffffffu, wd, b);
+            if (strict ? (d < bound) : (d <= bound)) {  // the bound may have shrunk
+                d_out = d;
+                return __shfl_sync(0xffffffffu, wst, b);
             }
         }
-        const unsigned hit = __ballot_sync(0xffffffffu, take);
-        if (hit) {
-            const int first = __ffs(hit) - 1;
-            spos += first + 1;
-            return __shfl_sync(0xffffffffu, st, first);
-        }
-        spos += 32;
     }
-    return -1;
+};
+
+template <int DP, int NSLOT>
+struct Ring {
+    float buf[NSLOT][kSub * DP];
+    uint64_t full[NSLOT];
+};
+
+template <int DP, int NSLOT>
+__device__ __forceinline__ void ring_issue(Ring<DP, NSLOT> &ring, int slot, const float *src) {
+    constexpr uint32_t bytes = kSub * DP * sizeof(float);
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&ring.full[slot], bytes);
+    bulk_g2s(ring.buf[slot], src, bytes, &ring.full[slot]);
 }
 
 // ---------------------------------------------------------------------------
 // pass 1: fp32 k-th neighbour distance (self included as the (k+1)-th slot)
-// refs: warp w owns sorted rows r0 + w*128 + r*32 + lane, r < kRT
+// lane l owns sorted rows wrow + r*32 + l, r < kRT
 // ---------------------------------------------------------------------------
-template <int D, int S>
-__global__ void __launch_bounds__(kNT) knn_pass_kernel(
-    const float *__restrict__ pts32, const float *__restrict__ box32,
-    const float *__restrict__ box128, const ChunkInfo *__restrict__ info,
-    const TileRef *__restrict__ tiles, int k, int prune, float *__restrict__ t32_out,
-    int32_t *__restrict__ L_out, unsigned long long *__restrict__ work) {
-    constexpr int DP = (D + 3) & ~3;
-    __shared__ __align__(128) Ring<DP> ring;
-    __shared__ float wbox[kWarps][2 * DP];
-    __shared__ float wbound[kWarps];
-    __shared__ int sid[2];
+template <int DY, int DX, int S>
+__global__ void __launch_bounds__(32) knn_pass_kernel(
+    const float *__restrict__ pts32, const float *__restrict__ fbox,
+    const ChunkInfo *__restrict__ info, const TileRef *__restrict__ tiles, int k, int prune,
+    float *__restrict__ t32_out, int32_t *__restrict__ L_out, unsigned long long *__restrict__ work) {
+    using L = Lay<DY, DX>;
+    constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG, NSLOT = L::NSLOT;
+    __shared__ __align__(128) Ring<DP, NSLOT> ring;
     const TileRef tr = tiles[blockIdx.x];
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x;
     const float *cp = pts32 + ci.prow0 * DP;
-    const int64_t sub0 = ci.prow0 / kSub, stage0 = ci.prow0 / kTJ;
-    Trav tv;
-    tv.init(tr.r0, ci.n, ci.npad);
-    const int wrow = tr.r0 + warp * kTJ;  // first sorted row of this warp
-    const bool wvalid = wrow < ci.n;
-    for (int e = lane; e < 2 * DP; e += 32)
-        wbox[warp][e] = wvalid ? box128[(stage0 + wrow / kTJ) * 2 * DP + e]
-                               : (e < DP ? INFINITY : -INFINITY);
-    if (lane == 0) wbound[warp] = wvalid ? INFINITY : 0.0f;
-    Ref<D> ref[kRT];
+    const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2;
+    const int wrow = tr.r0;
+    float2 ref[kRT][NP];
     float kd[kRT][S];
 #pragma unroll
     for (int r = 0; r < kRT; ++r) {
@@ -445,135 +435,110 @@ __global__ void __launch_bounds__(kNT) knn_pass_kernel(
         const bool valid = idx < ci.n;
         load_ref<D>(ref[r], cp + (int64_t)idx * DP, valid);
 #pragma unroll
-        for (int s = 0; s < S; ++s)
-            kd[r][s] = (!valid || s < S - (k + 1)) ? -INFINITY : INFINITY;
+        for (int s = 0; s < S; ++s) kd[r][s] = (!valid || s < S - (k + 1)) ? -INFINITY : INFINITY;
     }
-    if (threadIdx.x == 0) {
-        mbar_init(&ring.full[0], 1);
-        mbar_init(&ring.full[1], 1);
-        fence_barrier_init();
+    if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
+    fence_barrier_init();
+    __syncwarp();
+    Walker wk;
+    wk.init(fb, wrow, ci.n, ci.npad);
+    float bound = INFINITY;  // warp max of the current k-th distances
+    int slot_st = -1;        // lane s: sub-tile in ring slot s
+    int issued = 0;
+    uint32_t nsub = 0;
+    for (; issued < NSLOT; ++issued) {
+        float d;
+        const int st = wk.next(fb, prune ? bound : INFINITY, true, d);
+        if (st < 0) break;
+        if (lane == issued) slot_st = st;
+        if (lane == 0) ring_issue(ring, issued, cp + (int64_t)st * kSub * DP);
     }
-    __syncthreads();
-    int spos = 0;
-    if (warp == 0) {
-        for (int b = 0; b < 2; ++b) {
-            const int st = next_stage<DP>(tv, spos, box128, stage0, wbox, wbound, 0, D, true, prune);
-            if (lane == 0) {
-                sid[b] = st;
-                if (st >= 0) ring_issue(ring, b, cp + (int64_t)st * kTJ * DP);
-            }
-        }
-    }
-    __syncthreads();
-    uint32_t uses = 0;  // bit b: parity of buffer b
-    uint32_t nsub = 0;  // sub-tiles this warp evaluated
-    for (int it = 0;; ++it) {
-        const int b = it & 1;
-        const int cur = sid[b];
-        if (cur < 0) break;
-        mbar_wait(&ring.full[b], (uses >> b) & 1u);
-        uses ^= 1u << b;
-        const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[b]);
-        for (int q = 0; q < kSubPerStage; ++q) {
-            if (prune) {
-                float wb = 0.0f;
+    for (int used = 0; used < issued; ++used) {
+        const int slot = used % NSLOT;
+        mbar_wait(&ring.full[slot], (uint32_t)(used / NSLOT) & 1u);
+        const float2 *tile = reinterpret_cast<const float2 *>(ring.buf[slot]);
+#pragma unroll 1
+        for (int j = 0; j < kSub; ++j) {
+            const float2 *c = tile + j * (DP / 2);
+            constexpr int G = 2 * PG < D ? 2 * PG : D;  // gate columns 0 .. G-1
+            float a[kRT][2 * NP];
+            float dj[kRT];
+            bool need = false;
 #pragma unroll
-                for (int r = 0; r < kRT; ++r) wb = fmaxf(wb, kd[r][S - 1]);
-                wb = warp_max_nonneg(wb);
-                const float bd = box_dist<DP>(wbox[warp], box32 + (sub0 + (int64_t)cur * kSubPerStage + q) * 2 * DP, 0, D);
-                if (!(bd < wb)) continue;
+            for (int r = 0; r < kRT; ++r) {
+                diff_pairs<D, 0, PG>(ref[r], c, a[r]);
+                dj[r] = maxabs0<0, G, 2 * NP>(a[r]);
+                need |= dj[r] < kd[r][S - 1];
             }
-            ++nsub;
-#pragma unroll 2
-            for (int jj = 0; jj < kSub; ++jj) {
-                const int j = q * kSub + jj;
-                Cand<D> c;
-#pragma unroll
-                for (int v = 0; v < DP / 4; ++v) c.v[v] = tile[j * (DP / 4) + v];
-                float d[kRT];
-                bool any = false;
+            if (__any_sync(0xffffffffu, need)) {
+                bool ins = false;
 #pragma unroll
                 for (int r = 0; r < kRT; ++r) {
-                    float a[D];
-                    diffs<D>(ref[r], c, a);
-                    d[r] = maxabs0<0, D, D>(a);
-                    any |= d[r] < kd[r][S - 1];
+                    diff_pairs<D, PG, NP>(ref[r], c, a[r]);
+                    dj[r] = maxabs<G, D, 2 * NP>(a[r], dj[r]);
+                    ins |= dj[r] < kd[r][S - 1];
                 }
-                if (any) {
+                if (ins) {
 #pragma unroll
-                    for (int r = 0; r < kRT; ++r) insert_sorted<S>(kd[r], d[r]);
+                    for (int r = 0; r < kRT; ++r) insert_sorted<S>(kd[r], dj[r]);
                 }
             }
         }
-        {
-            float wb = 0.0f;
+        ++nsub;
+        float wb = 0.0f;
 #pragma unroll
-            for (int r = 0; r < kRT; ++r) wb = fmaxf(wb, kd[r][S - 1]);
-            wb = warp_max_nonneg(wb);
-            if (lane == 0 && wvalid) wbound[warp] = wb;
+        for (int r = 0; r < kRT; ++r) wb = fmaxf(wb, kd[r][S - 1]);
+        bound = warp_max_nonneg(wb);
+        __syncwarp();
+        float d;
+        const int st = wk.next(fb, prune ? bound : INFINITY, true, d);
+        if (st >= 0) {
+            if (lane == issued % NSLOT) slot_st = st;
+            if (lane == 0) ring_issue(ring, issued % NSLOT, cp + (int64_t)st * kSub * DP);
+            ++issued;
         }
-        __syncthreads();
-        if (warp == 0) {
-            const int st = next_stage<DP>(tv, spos, box128, stage0, wbox, wbound, 0, D, true, prune);
-            if (lane == 0) {
-                sid[b] = st;
-                if (st >= 0) ring_issue(ring, b, cp + (int64_t)st * kTJ * DP);
-            }
-        }
-        __syncthreads();
     }
-    if (lane == 0 && wvalid) atomicAdd(work, (unsigned long long)nsub);
+    (void)slot_st;
+    if (lane == 0) atomicAdd(work, (unsigned long long)nsub);
 #pragma unroll
     for (int r = 0; r < kRT; ++r) {
         const int idx = wrow + r * 32 + lane;
         if (idx >= ci.n) continue;
         const float t32 = kd[r][S - 1];
         const float lo = __double2float_rd(__dsub_rd((double)t32, 2.0 * ci.delta));
-        int L = 0;
+        int Lc = 0;
 #pragma unroll
-        for (int s = 0; s < S; ++s) L += (kd[r][s] > -INFINITY) && (kd[r][s] < lo);
-        if (lo > 0.0f) L -= 1;  // the self pair (distance 0) was counted
+        for (int s = 0; s < S; ++s) Lc += (kd[r][s] > -INFINITY) && (kd[r][s] < lo);
+        if (lo > 0.0f) Lc -= 1;  // the self pair (distance 0) was counted
         t32_out[ci.row0 + idx] = t32;
-        L_out[ci.row0 + idx] = L;
+        L_out[ci.row0 + idx] = Lc;
     }
 }
 
 // ---------------------------------------------------------------------------
 // pass 2: certain counts in the three TE marginals + band events
-//   columns: 0 = y_t, 1..DY = y-past, DY+1..D-1 = x-past (embedding.py:50-60)
-//   marginal 0 = y-past (A), 1 = y + y-past, 2 = y-past + x-past
-//   pruning uses the filter columns [f0, f0 + nf): a subset of every
-//   requested marginal and of the joint, so their box distance bounds all
-//   values that can count or fall in the band
+//   marginal 0 = y-past (A), 1 = y + y-past (m2), 2 = y-past + x-past (m3)
+//   A <= every marginal and the joint, so A > hi settles a pair (outside
+//   everywhere, no event) after the gate columns alone
 // ---------------------------------------------------------------------------
 template <int DY, int DX>
-__global__ void __launch_bounds__(kNT) count_pass_kernel(
-    const float *__restrict__ pts32, const float *__restrict__ box32,
-    const float *__restrict__ box128, const ChunkInfo *__restrict__ info,
-    const TileRef *__restrict__ tiles, const float *__restrict__ t32_in, int64_t ws_rows,
-    FilterCols fc, int prune, int32_t *__restrict__ cnt_out, uint32_t *__restrict__ ev,
-    int32_t *__restrict__ ev_n, uint32_t fmask, unsigned long long *__restrict__ work) {
-    constexpr int D = 1 + DY + DX;
-    constexpr int DP = (D + 3) & ~3;
-    __shared__ __align__(128) Ring<DP> ring;
-    __shared__ float wbox[kWarps][2 * DP];
-    __shared__ float wbound[kWarps];
-    __shared__ int sid[2];
+__global__ void __launch_bounds__(32) count_pass_kernel(
+    const float *__restrict__ pts32, const float *__restrict__ fbox,
+    const ChunkInfo *__restrict__ info, const TileRef *__restrict__ tiles,
+    const float *__restrict__ t32_in, int64_t ws_rows, int prune, int32_t *__restrict__ cnt_out,
+    uint32_t *__restrict__ ev, int32_t *__restrict__ ev_n, uint32_t fmask,
+    unsigned long long *__restrict__ work) {
+    using L = Lay<DY, DX>;
+    constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG, NSLOT = L::NSLOT;
+    __shared__ __align__(128) Ring<DP, NSLOT> ring;
     const TileRef tr = tiles[blockIdx.x];
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x;
     const float *cp = pts32 + ci.prow0 * DP;
-    const int64_t sub0 = ci.prow0 / kSub, stage0 = ci.prow0 / kTJ;
-    const int c0 = fc.f0, c1 = fc.f0 + fc.nf;
-    Trav tv;
-    tv.init(tr.r0, ci.n, ci.npad);
-    const int wrow = tr.r0 + warp * kTJ;
-    const bool wvalid = wrow < ci.n;
-    for (int e = lane; e < 2 * DP; e += 32)
-        wbox[warp][e] = wvalid ? box128[(stage0 + wrow / kTJ) * 2 * DP + e]
-                               : (e < DP ? INFINITY : -INFINITY);
-    Ref<D> ref[kRT];
+    const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2;
+    const int wrow = tr.r0;
+    float2 ref[kRT][NP];
     Band band[kRT];
     uint32_t cA[kRT], c2[kRT], c3[kRT];
     int nev[kRT];
@@ -595,103 +560,93 @@ __global__ void __launch_bounds__(kNT) count_pass_kernel(
         cA[r] = c2[r] = c3[r] = 0;
         nev[r] = 0;
     }
-    const float wb = warp_max_nonneg(hmax);
-    if (lane == 0) wbound[warp] = wvalid ? wb : -1.0f;
-    if (threadIdx.x == 0) {
-        mbar_init(&ring.full[0], 1);
-        mbar_init(&ring.full[1], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-    int spos = 0;
-    if (warp == 0) {
-        for (int b = 0; b < 2; ++b) {
-            const int st = next_stage<DP>(tv, spos, box128, stage0, wbox, wbound, c0, c1, false, prune);
-            if (lane == 0) {
-                sid[b] = st;
-                if (st >= 0) ring_issue(ring, b, cp + (int64_t)st * kTJ * DP);
-            }
-        }
-    }
-    __syncthreads();
-    uint32_t uses = 0;
+    const float bound = warp_max_nonneg(hmax);
+    if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
+    fence_barrier_init();
+    __syncwarp();
+    Walker wk;
+    wk.init(fb, wrow, ci.n, ci.npad);
+    int slot_st = -1;
+    int issued = 0;
     uint32_t nsub = 0;
-    for (int it = 0;; ++it) {
-        const int b = it & 1;
-        const int cur = sid[b];
-        if (cur < 0) break;
-        mbar_wait(&ring.full[b], (uses >> b) & 1u);
-        uses ^= 1u << b;
-        const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[b]);
-        for (int q = 0; q < kSubPerStage; ++q) {
-            if (prune) {
-                const float bd = box_dist<DP>(wbox[warp], box32 + (sub0 + (int64_t)cur * kSubPerStage + q) * 2 * DP, c0, c1);
-                if (!(bd <= wb) || !wvalid) continue;
-            }
-            ++nsub;
+    for (; issued < NSLOT; ++issued) {
+        float d;
+        const int st = wk.next(fb, prune ? bound : INFINITY, false, d);
+        if (st < 0) break;
+        if (lane == issued) slot_st = st;
+        if (lane == 0) ring_issue(ring, issued, cp + (int64_t)st * kSub * DP);
+    }
+    for (int used = 0; used < issued; ++used) {
+        const int slot = used % NSLOT;
+        const int cur = __shfl_sync(0xffffffffu, slot_st, slot);
+        mbar_wait(&ring.full[slot], (uint32_t)(used / NSLOT) & 1u);
+        const float2 *tile = reinterpret_cast<const float2 *>(ring.buf[slot]);
 #pragma unroll 1
-            for (int jj = 0; jj < kSub; ++jj) {
-                const int j = q * kSub + jj;
-                Cand<D> c;
+        for (int j = 0; j < kSub; ++j) {
+            const float2 *c = tile + j * (DP / 2);
+            float a[kRT][2 * NP];
+            float vA[kRT];
+            bool need = false;
 #pragma unroll
-                for (int v = 0; v < DP / 4; ++v) c.v[v] = tile[j * (DP / 4) + v];
-                float vA[kRT], v2[kRT], v3[kRT], vj[kRT];
-                bool any = false;
+            for (int r = 0; r < kRT; ++r) {
+                diff_pairs<D, 0, PG>(ref[r], c, a[r]);
+                vA[r] = maxabs0<1, 1 + DY, 2 * NP>(a[r]);
+                need |= vA[r] <= band[r].hi;
+            }
+            if (!__any_sync(0xffffffffu, need)) continue;
+            float v2[kRT], v3[kRT], vj[kRT];
+            bool any = false;
+#pragma unroll
+            for (int r = 0; r < kRT; ++r) {
+                diff_pairs<D, PG, NP>(ref[r], c, a[r]);
+                const float A = vA[r];
+                const float m2 = fmaxf(A, fabsf(a[r][0]));
+                const float m3 = maxabs<1 + DY, D, 2 * NP>(a[r], A);
+                const float jd = fmaxf(m2, m3);
+                // certain-inside counts: sign bit of (v - lo)
+                const float2 e = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nlo, band[r].nlo));
+                const float e3 = m3 + band[r].nlo;
+                cA[r] += __float_as_uint(e.x) >> 31;
+                c2[r] += __float_as_uint(e.y) >> 31;
+                c3[r] += __float_as_uint(e3) >> 31;
+                // conservative band test: min |v - t| <= w
+                const float2 b1 = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nt, band[r].nt));
+                const float2 b2 = __fadd2_rn(make_float2(m3, jd), make_float2(band[r].nt, band[r].nt));
+                const float bm = fminf(fminf(fabsf(b1.x), fabsf(b1.y)), fminf(fabsf(b2.x), fabsf(b2.y)));
+                any |= bm <= band[r].w;
+                v2[r] = m2;
+                v3[r] = m3;
+                vj[r] = jd;
+            }
+            if (any) {
+                const int jg = cur * kSub + j;
 #pragma unroll
                 for (int r = 0; r < kRT; ++r) {
-                    float a[D];
-                    diffs<D>(ref[r], c, a);
-                    const float A = maxabs0<1, 1 + DY, D>(a);
-                    const float m2 = fmaxf(A, fabsf(a[0]));
-                    const float m3 = maxabs<1 + DY, D, D>(a, A);
-                    const float jd = fmaxf(m2, m3);
-                    // certain-inside counts: sign bit of (v - lo)
-                    const float2 e = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nlo, band[r].nlo));
-                    const float e3 = m3 + band[r].nlo;
-                    cA[r] += __float_as_uint(e.x) >> 31;
-                    c2[r] += __float_as_uint(e.y) >> 31;
-                    c3[r] += __float_as_uint(e3) >> 31;
-                    // conservative band test: min |v - t| <= w
-                    const float2 b1 = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nt, band[r].nt));
-                    const float2 b2 = __fadd2_rn(make_float2(m3, jd), make_float2(band[r].nt, band[r].nt));
-                    const float bm = fminf(fminf(fabsf(b1.x), fabsf(b1.y)), fminf(fabsf(b2.x), fabsf(b2.y)));
-                    any |= bm <= band[r].w;
-                    vA[r] = A;
-                    v2[r] = m2;
-                    v3[r] = m3;
-                    vj[r] = jd;
-                }
-                if (any) {
-                    const int jg = cur * kTJ + j;
-#pragma unroll
-                    for (int r = 0; r < kRT; ++r) {
-                        const float lo = band[r].lo, hi = band[r].hi;
-                        uint32_t f = ((vA[r] >= lo && vA[r] <= hi) ? 1u : 0u) |
-                                     ((v2[r] >= lo && v2[r] <= hi) ? 2u : 0u) |
-                                     ((v3[r] >= lo && v3[r] <= hi) ? 4u : 0u) |
-                                     ((vj[r] >= lo && vj[r] <= hi) ? 8u : 0u);
-                        f &= fmask;
-                        if (f) {
-                            const int idx = wrow + r * 32 + lane;
-                            if (nev[r] < kCap)
-                                ev[(ci.row0 + idx) * kCap + nev[r]] = (uint32_t)jg | (f << 28);
-                            ++nev[r];
-                        }
+                    const float lo = band[r].lo, hi = band[r].hi;
+                    uint32_t f = ((vA[r] >= lo && vA[r] <= hi) ? 1u : 0u) |
+                                 ((v2[r] >= lo && v2[r] <= hi) ? 2u : 0u) |
+                                 ((v3[r] >= lo && v3[r] <= hi) ? 4u : 0u) |
+                                 ((vj[r] >= lo && vj[r] <= hi) ? 8u : 0u);
+                    f &= fmask;
+                    if (f) {
+                        const int idx = wrow + r * 32 + lane;
+                        if (nev[r] < kCap) ev[(ci.row0 + idx) * kCap + nev[r]] = (uint32_t)jg | (f << 28);
+                        ++nev[r];
                     }
                 }
             }
         }
-        __syncthreads();
-        if (warp == 0) {
-            const int st = next_stage<DP>(tv, spos, box128, stage0, wbox, wbound, c0, c1, false, prune);
-            if (lane == 0) {
-                sid[b] = st;
-                if (st >= 0) ring_issue(ring, b, cp + (int64_t)st * kTJ * DP);
-            }
+        ++nsub;
+        __syncwarp();
+        float d;
+        const int st = wk.next(fb, prune ? bound : INFINITY, false, d);
+        if (st >= 0) {
+            if (lane == issued % NSLOT) slot_st = st;
+            if (lane == 0) ring_issue(ring, issued % NSLOT, cp + (int64_t)st * kSub * DP);
+            ++issued;
         }
-        __syncthreads();
     }
-    if (lane == 0 && wvalid) atomicAdd(work, (unsigned long long)nsub);
+    if (lane == 0) atomicAdd(work, (unsigned long long)nsub);
 #pragma unroll
     for (int r = 0; r < kRT; ++r) {
         const int idx = wrow + r * 32 + lane;
@@ -707,6 +662,7 @@ __global__ void __launch_bounds__(kNT) count_pass_kernel(
 
 // ---------------------------------------------------------------------------
 // resolve: fp64 certification of band events (sorted positions -> rows via perm)
+// one thread per reference of a 128-reference tile
 // ---------------------------------------------------------------------------
 struct TeLayout {
     int dy;
@@ -729,7 +685,7 @@ __device__ __forceinline__ void te_dist64(const double *ref, const double *q, in
     jd = fmax(m2, m3);
 }
 
-__global__ void __launch_bounds__(kNT) resolve_kernel(
+__global__ void __launch_bounds__(kWarpRefs) resolve_kernel(
     const double *__restrict__ pts64, int dim, const ChunkInfo *__restrict__ info,
     const TileRef *__restrict__ tiles, int k, TeLayout lay, const int32_t *__restrict__ perm,
     const int32_t *__restrict__ L_in, const int32_t *__restrict__ cnt_in,
@@ -738,62 +694,60 @@ __global__ void __launch_bounds__(kNT) resolve_kernel(
     int64_t *__restrict__ ovf_list, int32_t *__restrict__ ovf_n) {
     const TileRef tr = tiles[blockIdx.x];
     const ChunkInfo ci = info[tr.chunk];
-    for (int r = 0; r < kRT; ++r) {
-        const int s = tr.r0 + r * kNT + threadIdx.x;  // sorted position
-        if (s >= ci.n) continue;
-        const int64_t srow = ci.row0 + s;
-        const int64_t row = ci.ok32 ? ci.row0 + perm[srow] : srow;
-        const int ne = ci.ok32 ? ev_n[srow] : kCap + 1;
-        const int need = ci.ok32 ? k - L_in[srow] : 0;
-        bool fallback = !ci.ok32 || ne > kCap || need < 1;
-        double eps = 0.0;
-        int extra[3] = {0, 0, 0};
-        if (!fallback) {
-            double ref[kMaxDim];
-            const double *rp = pts64 + row * dim;
-            for (int c = 0; c < dim; ++c) ref[c] = rp[c];
-            double dj[kCap];
-            int nj = 0;
+    const int s = tr.r0 + threadIdx.x;  // sorted position
+    if (s >= ci.n) return;
+    const int64_t srow = ci.row0 + s;
+    const int64_t row = ci.ok32 ? ci.row0 + perm[srow] : srow;
+    const int ne = ci.ok32 ? ev_n[srow] : kCap + 1;
+    const int need = ci.ok32 ? k - L_in[srow] : 0;
+    bool fallback = !ci.ok32 || ne > kCap || need < 1;
+    double eps = 0.0;
+    int extra[3] = {0, 0, 0};
+    if (!fallback) {
+        double ref[kMaxDim];
+        const double *rp = pts64 + row * dim;
+        for (int c = 0; c < dim; ++c) ref[c] = rp[c];
+        double dj[kCap];
+        int nj = 0;
+        for (int e = 0; e < ne; ++e) {
+            const uint32_t w = ev[srow * kCap + e];
+            const int j = (int)(w & 0x0FFFFFFFu);
+            if (j == s || !(w >> 31)) continue;
+            double A, m2, m3, jd;
+            te_dist64(ref, pts64 + (ci.row0 + perm[ci.row0 + j]) * dim, dim, lay.dy, A, m2, m3, jd);
+            int p = nj++;
+            while (p > 0 && dj[p - 1] > jd) {
+                dj[p] = dj[p - 1];
+                --p;
+            }
+            dj[p] = jd;
+        }
+        if (need > nj) {
+            fallback = true;
+        } else {
+            eps = dj[need - 1];
             for (int e = 0; e < ne; ++e) {
                 const uint32_t w = ev[srow * kCap + e];
                 const int j = (int)(w & 0x0FFFFFFFu);
-                if (j == s || !(w >> 31)) continue;
+                const uint32_t f = (w >> 28) & 7u;
+                if (j == s || !f) continue;
                 double A, m2, m3, jd;
                 te_dist64(ref, pts64 + (ci.row0 + perm[ci.row0 + j]) * dim, dim, lay.dy, A, m2, m3, jd);
-                int p = nj++;
-                while (p > 0 && dj[p - 1] > jd) {
-                    dj[p] = dj[p - 1];
-                    --p;
-                }
-                dj[p] = jd;
-            }
-            if (need > nj) {
-                fallback = true;
-            } else {
-                eps = dj[need - 1];
-                for (int e = 0; e < ne; ++e) {
-                    const uint32_t w = ev[srow * kCap + e];
-                    const int j = (int)(w & 0x0FFFFFFFu);
-                    const uint32_t f = (w >> 28) & 7u;
-                    if (j == s || !f) continue;
-                    double A, m2, m3, jd;
-                    te_dist64(ref, pts64 + (ci.row0 + perm[ci.row0 + j]) * dim, dim, lay.dy, A, m2, m3, jd);
-                    extra[0] += (f & 1u) && (A < eps);
-                    extra[1] += (f & 2u) && (m2 < eps);
-                    extra[2] += (f & 4u) && (m3 < eps);
-                }
+                extra[0] += (f & 1u) && (A < eps);
+                extra[1] += (f & 2u) && (m2 < eps);
+                extra[2] += (f & 4u) && (m3 < eps);
             }
         }
-        if (fallback) {
-            const int slot = atomicAdd(ovf_n, 1);
-            ovf_list[slot] = row;
-            continue;
-        }
-        out_eps[row] = eps;
-        for (int o = 0; o < lay.nout; ++o) {
-            const int sl = lay.slot[o];
-            out_counts[o * total_rows + row] = cnt_in[sl * ws_rows + srow] + extra[sl];
-        }
+    }
+    if (fallback) {
+        const int slot = atomicAdd(ovf_n, 1);
+        ovf_list[slot] = row;
+        return;
+    }
+    out_eps[row] = eps;
+    for (int o = 0; o < lay.nout; ++o) {
+        const int sl = lay.slot[o];
+        out_counts[o * total_rows + row] = cnt_in[sl * ws_rows + srow] + extra[sl];
     }
 }
 
@@ -892,42 +846,33 @@ __global__ void __launch_bounds__(kExactWarps * 32) exact_kernel(
 // ---------------------------------------------------------------------------
 // host side: kernel tables and dispatch
 // ---------------------------------------------------------------------------
-using KnnFn = void (*)(const float *, const float *, const float *, const ChunkInfo *,
-                       const TileRef *, int, int, float *, int32_t *, unsigned long long *);
-using CountFn = void (*)(const float *, const float *, const float *, const ChunkInfo *,
-                         const TileRef *, const float *, int64_t, FilterCols, int, int32_t *,
-                         uint32_t *, int32_t *, uint32_t, unsigned long long *);
+using KnnFn = void (*)(const float *, const float *, const ChunkInfo *, const TileRef *, int, int,
+                       float *, int32_t *, unsigned long long *);
+using CountFn = void (*)(const float *, const float *, const ChunkInfo *, const TileRef *,
+                         const float *, int64_t, int, int32_t *, uint32_t *, int32_t *, uint32_t,
+                         unsigned long long *);
 
-template <int D>
-static KnnFn knn_for_slots(int slots) {
-    if (slots <= 5) return knn_pass_kernel<D, 5>;
-    if (slots <= 8) return knn_pass_kernel<D, 8>;
-    if (slots <= 16) return knn_pass_kernel<D, 16>;
-    return nullptr;
-}
-
-static KnnFn knn_table(int dim, int slots) {
-    switch (dim) {
-        case 3: return knn_for_slots<3>(slots);
-        case 4: return knn_for_slots<4>(slots);
-        case 5: return knn_for_slots<5>(slots);
-        case 6: return knn_for_slots<6>(slots);
-        case 7: return knn_for_slots<7>(slots);
-        case 8: return knn_for_slots<8>(slots);
-        case 9: return knn_for_slots<9>(slots);
-        case 11: return knn_for_slots<11>(slots);
-        case 13: return knn_for_slots<13>(slots);
-        case 15: return knn_for_slots<15>(slots);
-        case 17: return knn_for_slots<17>(slots);
-        default: return nullptr;
-    }
-}
-
-// (DY, DX) layouts with a compiled count kernel: TE embeddings d_y, d_x <= 3,
-// the symmetric C3 sweep (1+2d) and the bench layout (marginal = first m cols).
+// (DY, DX) layouts with compiled sweeps: TE embeddings d_y, d_x <= 3, the
+// symmetric C3 sweep (1+2d) and the bench layout (marginal = first m cols).
 #define ENTE_TE_LAYOUTS(X)                                                                  \
     X(1, 1) X(1, 2) X(2, 1) X(2, 2) X(1, 3) X(3, 1) X(2, 3) X(3, 2) X(3, 3) X(4, 4) X(5, 5) \
     X(6, 6) X(7, 7) X(8, 8) X(0, 2) X(1, 4) X(2, 4) X(3, 5) X(4, 6) X(5, 7) X(6, 8) X(7, 9)
+
+template <int DY, int DX>
+static KnnFn knn_for_slots(int slots) {
+    if (slots <= 5) return knn_pass_kernel<DY, DX, 5>;
+    if (slots <= 8) return knn_pass_kernel<DY, DX, 8>;
+    if (slots <= 16) return knn_pass_kernel<DY, DX, 16>;
+    return nullptr;
+}
+
+static KnnFn knn_table(int dy, int dx, int slots) {
+#define ENTE_CASE(a, b) \
+    if (dy == a && dx == b) return knn_for_slots<a, b>(slots);
+    ENTE_TE_LAYOUTS(ENTE_CASE)
+#undef ENTE_CASE
+    return nullptr;
+}
 
 static CountFn count_table(int dy, int dx) {
 #define ENTE_CASE(a, b) \
@@ -952,7 +897,9 @@ struct Plan {
 static bool match_te_layout(int dim, const uint32_t *masks, int n_marg, int &dy_out,
                             TeLayout &lay) {
     const uint32_t all_but_0 = ((dim >= 32) ? 0xFFFFFFFFu : ((1u << dim) - 1u)) & ~1u;
-    for (int dy = 0; dy < dim; ++dy) {
+    // with no marginals any layout of the right width serves (the gate is then
+    // only a lower bound of the joint distance): prefer a y-past block
+    for (int dy = n_marg == 0 ? 1 : 0; dy < dim; ++dy) {
         const uint32_t yp = ((1u << (dy + 1)) - 1u) & ~1u;  // cols 1..dy
         const uint32_t yyp = (1u << (dy + 1)) - 1u;         // cols 0..dy
         bool ok = true;
@@ -972,23 +919,14 @@ static bool match_te_layout(int dim, const uint32_t *masks, int n_marg, int &dy_
     return false;
 }
 
-// Filter columns: the intersection of every requested marginal with the
-// joint, as a contiguous range (the TE marginals are ranges sharing y-past).
-static FilterCols filter_cols(int dim, int dy, const TeLayout &lay) {
-    int lo = 0, hi = dim;
-    for (int o = 0; o < lay.nout; ++o) {
-        switch (lay.slot[o]) {
-            case 0: lo = std::max(lo, 1); hi = std::min(hi, dy + 1); break;
-            case 1: hi = std::min(hi, dy + 1); break;
-            default: lo = std::max(lo, 1); break;
-        }
-    }
+// Gate / filter columns: the y-past block [1, 1 + dy), a subset of every TE
+// marginal and of the joint (embedding.py:50-60), capped at kGate columns
+// for the Morton key and the sub-tile boxes.
+static FilterCols filter_cols(int dy) {
     FilterCols fc{};
-    fc.f0 = lo;
-    fc.nf = std::max(0, hi - lo);
+    fc.f0 = 1;
+    fc.nf = std::min(dy, kGate);
     fc.bits = fc.nf > 0 ? std::min(10, 30 / fc.nf) : 0;
-    if (fc.nf > 0 && fc.bits == 0) fc.bits = 1;  // nf > 30: one bit per column
-    if (fc.nf * fc.bits > 32) fc.nf = 32 / fc.bits;  // Morton over a prefix
     return fc;
 }
 
@@ -1009,18 +947,19 @@ static Plan make_plan(const ente_chunk *chunks, int n_chunks, int dim, const uin
         const int npad = round_up(chunks[c].n, kTJ);
         p.total_prows += npad;
         p.max_npad = std::max(p.max_npad, npad);
-        p.n_tiles += (chunks[c].n + kRefTile - 1) / kRefTile;
+        p.n_tiles += (chunks[c].n + kWarpRefs - 1) / kWarpRefs;
     }
     int dy = 0;
     TeLayout lay{};
-    if (k + 1 <= 16 && knn_table(dim, k + 1) && match_te_layout(dim, masks, n_marg, dy, lay)) {
+    if (k + 1 <= 16 && match_te_layout(dim, masks, n_marg, dy, lay) &&
+        knn_table(dy, dim - 1 - dy, k + 1)) {
         p.fast = true;
         p.dy = dy;
         p.dx = dim - 1 - dy;
         p.slots = k + 1;
         p.dp = (dim + 3) & ~3;
         p.lay = lay;
-        p.fc = filter_cols(dim, dy, lay);
+        p.fc = filter_cols(dy);
     }
     return p;
 }
@@ -1030,8 +969,7 @@ struct SearchWs {
     ColStats *stats;
     TileRef *tiles;
     float *pts32;
-    float *box32;
-    float *box128;
+    float *fbox;
     uint32_t *ka, *kb;
     int32_t *va, *vb;
     int32_t *perm;
@@ -1052,8 +990,7 @@ static SearchWs layout_ws(Arena &a, const Plan &p, int n_chunks) {
         w.stats = a.take<ColStats>(n_chunks);
         w.tiles = a.take<TileRef>(p.n_tiles);
         w.pts32 = a.take<float>((size_t)p.total_prows * p.dp);
-        w.box32 = a.take<float>((size_t)(p.total_prows / kSub) * 2 * p.dp);
-        w.box128 = a.take<float>((size_t)(p.total_prows / kTJ) * 2 * p.dp);
+        w.fbox = a.take<float>((size_t)(p.total_prows / kSub) * 2 * kGate);
         w.ka = a.take<uint32_t>(p.total_rows);
         w.kb = a.take<uint32_t>(p.total_rows);
         w.va = a.take<int32_t>(p.total_rows);
@@ -1155,7 +1092,7 @@ extern "C" size_t ente_search_workspace_size(const ente_chunk *chunks, int n_chu
     uint32_t dummy[kMaxMarg] = {0};
     Plan p = make_plan(chunks, n_chunks, dim, dummy, 0, k);
     // size for the fast path whenever it could be taken
-    if (k + 1 <= 16 && knn_table(dim, k + 1)) {
+    if (k + 1 <= 16) {
         p.fast = true;
         p.dp = (dim + 3) & ~3;
     }
@@ -1228,7 +1165,7 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
         prow += ci.npad;
         if (k > ci.n - 1) hstatus[c] = ENTE_CHUNK_K_TOO_LARGE;
         if (p.fast && hstatus[c] == ENTE_CHUNK_OK)
-            for (int r0 = 0; r0 < ci.n; r0 += kRefTile) htiles.push_back({c, r0});
+            for (int r0 = 0; r0 < ci.n; r0 += kWarpRefs) htiles.push_back({c, r0});
     }
     ENTE_CUDA(cudaMemcpyAsync(w.info, hinfo.data(), sizeof(ChunkInfo) * n_chunks,
                               cudaMemcpyHostToDevice, st));
@@ -1257,27 +1194,25 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
         dim3 ggrid((unsigned)(p.max_npad / kTJ), (unsigned)std::min(n_chunks, 65535));
         ENTE_LAUNCH("gather", st,
                     gather_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.stats,
-                                                         w.perm, p.dp, w.pts32, w.box32,
-                                                         w.box128));
+                                                         w.perm, p.dp, p.fc, w.pts32, w.fbox));
         ENTE_CUDA(cudaGetLastError());
         ENTE_CUDA(cudaMemcpyAsync(w.tiles, htiles.data(), sizeof(TileRef) * htiles.size(),
                                   cudaMemcpyHostToDevice, st));
         const unsigned nt = (unsigned)htiles.size();
         ENTE_LAUNCH("knn_pass", st,
-                    knn_table(dim, p.slots)<<<nt, kNT, 0, st>>>(w.pts32, w.box32, w.box128, w.info,
-                                                               w.tiles, k, prune, w.t32, w.L,
-                                                               work));
+                    knn_table(p.dy, p.dx, p.slots)<<<nt, 32, 0, st>>>(w.pts32, w.fbox, w.info,
+                                                                     w.tiles, k, prune, w.t32,
+                                                                     w.L, work));
         ENTE_CUDA(cudaGetLastError());
         uint32_t fmask = 8u;
         for (int o = 0; o < p.lay.nout; ++o) fmask |= 1u << p.lay.slot[o];
         ENTE_LAUNCH("count_pass", st,
-                    count_table(p.dy, p.dx)<<<nt, kNT, 0, st>>>(w.pts32, w.box32, w.box128, w.info,
-                                                                w.tiles, w.t32, ws_rows, p.fc,
-                                                                prune, w.cnt3, w.ev, w.ev_n, fmask,
-                                                                work + 1));
+                    count_table(p.dy, p.dx)<<<nt, 32, 0, st>>>(w.pts32, w.fbox, w.info, w.tiles,
+                                                               w.t32, ws_rows, prune, w.cnt3, w.ev,
+                                                               w.ev_n, fmask, work + 1));
         ENTE_CUDA(cudaGetLastError());
         ENTE_LAUNCH("resolve", st,
-                    resolve_kernel<<<nt, kNT, 0, st>>>(pts64, dim, w.info, w.tiles, k, p.lay,
+                    resolve_kernel<<<nt, kWarpRefs, 0, st>>>(pts64, dim, w.info, w.tiles, k, p.lay,
                                                        w.perm, w.L, w.cnt3, w.ev, w.ev_n, ws_rows,
                                                        total_rows, out_eps, out_counts, w.ovf,
                                                        w.ovf_n));
