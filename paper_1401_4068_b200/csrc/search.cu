@@ -370,9 +370,13 @@ struct Walker {
         return fmaxf(fmaxf(a, b), 0.0f);
     }
 
-    // Next sub-tile whose box distance is below `bound` (strict) or not above
-    // it; returns -1 when the walk is over.
-    __device__ int next(const float4 *__restrict__ fb, float bound, bool strict, float &d_out) {
+    // Next sub-tile whose box distance to the warp's box is below `bound`
+    // (strict) or not above it, AND that some reference of the warp needs by
+    // its own point-to-box distance (refs_need(lo, hi), evaluated per lane);
+    // returns -1 when the walk is over.
+    template <class RefTest>
+    __device__ int next(const float4 *__restrict__ fb, float bound, bool strict,
+                        RefTest &&refs_need) {
         const int lane = threadIdx.x & 31;
         for (;;) {
             while (mask == 0) {
@@ -386,13 +390,31 @@ struct Walker {
             const int b = __ffs(mask) - 1;
             mask &= mask - 1;
             const float d = __shfl_sync(0xffffffffu, wd, b);
-            if (strict ? (d < bound) : (d <= bound)) {  // the bound may have shrunk
-                d_out = d;
-                return __shfl_sync(0xffffffffu, wst, b);
-            }
+            if (!(strict ? (d < bound) : (d <= bound))) continue;  // the bound may have shrunk
+            const int st = __shfl_sync(0xffffffffu, wst, b);
+            const float4 lo = __ldg(fb + 2 * st), hi = __ldg(fb + 2 * st + 1);
+            if (__any_sync(0xffffffffu, refs_need(lo, hi))) return st;
         }
     }
 };
+
+// fp32 distance from a reference (negated packed coordinates) to a sub-tile
+// box over the gate columns 1 .. NG (NG <= kGate): a lower bound of the
+// reference's fp32 distance to every row of the sub-tile (fl monotone).
+template <int NG, int NP>
+__device__ __forceinline__ float point_box(const float2 (&nr)[NP], float4 lo, float4 hi) {
+    const float l[4] = {lo.x, lo.y, lo.z, lo.w};
+    const float h[4] = {hi.x, hi.y, hi.z, hi.w};
+    float d = 0.0f;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        const int c = 1 + g;  // column
+        const float x = (c & 1) ? nr[c >> 1].y : nr[c >> 1].x;  // -x_c
+        const float2 e = __fadd2_rn(make_float2(l[g], h[g]), make_float2(x, x));  // lo-x, hi-x
+        d = fmaxf(fmaxf(d, e.x), -e.y);
+    }
+    return d;
+}
 
 template <int DP, int NSLOT>
 struct Ring {
@@ -442,13 +464,19 @@ __global__ void __launch_bounds__(32) knn_pass_kernel(
     __syncwarp();
     Walker wk;
     wk.init(fb, wrow, ci.n, ci.npad);
+    constexpr int NG = DY < kGate ? DY : kGate;
     float bound = INFINITY;  // warp max of the current k-th distances
+    auto refs_need = [&](float4 lo, float4 hi) {
+        bool need = !prune;
+#pragma unroll
+        for (int r = 0; r < kRT; ++r) need |= point_box<NG, NP>(ref[r], lo, hi) < kd[r][S - 1];
+        return need;
+    };
     int slot_st = -1;        // lane s: sub-tile in ring slot s
     int issued = 0;
     uint32_t nsub = 0;
     for (; issued < NSLOT; ++issued) {
-        float d;
-        const int st = wk.next(fb, prune ? bound : INFINITY, true, d);
+        const int st = wk.next(fb, prune ? bound : INFINITY, true, refs_need);
         if (st < 0) break;
         if (lane == issued) slot_st = st;
         if (lane == 0) ring_issue(ring, issued, cp + (int64_t)st * kSub * DP);
@@ -456,11 +484,22 @@ __global__ void __launch_bounds__(32) knn_pass_kernel(
     for (int used = 0; used < issued; ++used) {
         const int slot = used % NSLOT;
         mbar_wait(&ring.full[slot], (uint32_t)(used / NSLOT) & 1u);
-        const float2 *tile = reinterpret_cast<const float2 *>(ring.buf[slot]);
-#pragma unroll 1
+        const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[slot]);
+        constexpr int G = 2 * PG < D ? 2 * PG : D;  // gate columns 0 .. G-1
+        constexpr int NQ = DP / 4;
+        float4 nxt[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) nxt[q] = tile[q];
+#pragma unroll 2
         for (int j = 0; j < kSub; ++j) {
-            const float2 *c = tile + j * (DP / 2);
-            constexpr int G = 2 * PG < D ? 2 * PG : D;  // gate columns 0 .. G-1
+            float4 cur[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) cur[q] = nxt[q];
+            if (j + 1 < kSub) {  // prefetch the next candidate row
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) nxt[q] = tile[(j + 1) * NQ + q];
+            }
+            const float2 *c = reinterpret_cast<const float2 *>(cur);
             float a[kRT][2 * NP];
             float dj[kRT];
             bool need = false;
@@ -490,8 +529,7 @@ __global__ void __launch_bounds__(32) knn_pass_kernel(
         for (int r = 0; r < kRT; ++r) wb = fmaxf(wb, kd[r][S - 1]);
         bound = warp_max_nonneg(wb);
         __syncwarp();
-        float d;
-        const int st = wk.next(fb, prune ? bound : INFINITY, true, d);
+        const int st = wk.next(fb, prune ? bound : INFINITY, true, refs_need);
         if (st >= 0) {
             if (lane == issued % NSLOT) slot_st = st;
             if (lane == 0) ring_issue(ring, issued % NSLOT, cp + (int64_t)st * kSub * DP);
@@ -561,6 +599,13 @@ __global__ void __launch_bounds__(32) count_pass_kernel(
         nev[r] = 0;
     }
     const float bound = warp_max_nonneg(hmax);
+    constexpr int NG = DY < kGate ? DY : kGate;
+    auto refs_need = [&](float4 lo, float4 hi) {
+        bool need = !prune;
+#pragma unroll
+        for (int r = 0; r < kRT; ++r) need |= point_box<NG, NP>(ref[r], lo, hi) <= band[r].hi;
+        return need;
+    };
     if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
     fence_barrier_init();
     __syncwarp();
@@ -570,20 +615,30 @@ __global__ void __launch_bounds__(32) count_pass_kernel(
     int issued = 0;
     uint32_t nsub = 0;
     for (; issued < NSLOT; ++issued) {
-        float d;
-        const int st = wk.next(fb, prune ? bound : INFINITY, false, d);
+        const int st = wk.next(fb, prune ? bound : INFINITY, false, refs_need);
         if (st < 0) break;
         if (lane == issued) slot_st = st;
         if (lane == 0) ring_issue(ring, issued, cp + (int64_t)st * kSub * DP);
     }
     for (int used = 0; used < issued; ++used) {
         const int slot = used % NSLOT;
-        const int cur = __shfl_sync(0xffffffffu, slot_st, slot);
+        const int cur_st = __shfl_sync(0xffffffffu, slot_st, slot);
         mbar_wait(&ring.full[slot], (uint32_t)(used / NSLOT) & 1u);
-        const float2 *tile = reinterpret_cast<const float2 *>(ring.buf[slot]);
-#pragma unroll 1
+        const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[slot]);
+        constexpr int NQ = DP / 4;
+        float4 nxt[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) nxt[q] = tile[q];
+#pragma unroll 2
         for (int j = 0; j < kSub; ++j) {
-            const float2 *c = tile + j * (DP / 2);
+            float4 cur[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) cur[q] = nxt[q];
+            if (j + 1 < kSub) {  // prefetch the next candidate row
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) nxt[q] = tile[(j + 1) * NQ + q];
+            }
+            const float2 *c = reinterpret_cast<const float2 *>(cur);
             float a[kRT][2 * NP];
             float vA[kRT];
             bool need = false;
@@ -619,7 +674,7 @@ __global__ void __launch_bounds__(32) count_pass_kernel(
                 vj[r] = jd;
             }
             if (any) {
-                const int jg = cur * kSub + j;
+                const int jg = cur_st * kSub + j;
 #pragma unroll
                 for (int r = 0; r < kRT; ++r) {
                     const float lo = band[r].lo, hi = band[r].hi;
@@ -638,8 +693,7 @@ __global__ void __launch_bounds__(32) count_pass_kernel(
         }
         ++nsub;
         __syncwarp();
-        float d;
-        const int st = wk.next(fb, prune ? bound : INFINITY, false, d);
+        const int st = wk.next(fb, prune ? bound : INFINITY, false, refs_need);
         if (st >= 0) {
             if (lane == issued % NSLOT) slot_st = st;
             if (lane == 0) ring_issue(ring, issued % NSLOT, cp + (int64_t)st * kSub * DP);
