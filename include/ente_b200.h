@@ -142,6 +142,15 @@ int ente_pack_te(const double *x, const double *y, int reps, int n_samples, int 
                  int dy, int tau_y, int t_lo, int t_hi, const int32_t *items, int n_items,
                  const int32_t *perms, double *out, void *stream);
 
+/* ente_pack_te_items -- the same gather with a window per item (the delay
+ * scan x surrogates x time points of a non-stationary analysis in one
+ * launch): items [host] n_items x 3 int32 {u, perm_index, t_lo}, every
+ * window w samples wide.  Replaces one assemble_pointsets call per
+ * (window, u) (embedding.py:75-120). */
+int ente_pack_te_items(const double *x, const double *y, int reps, int n_samples, int dx,
+                       int tau_x, int dy, int tau_y, int w, const int32_t *items, int n_items,
+                       const int32_t *perms, double *out, void *stream);
+
 /* ---------------------------------------------------------------------------
  * ente_te_reduce -- KSG transfer entropy of each TE-layout chunk:
  *   te = psi(k) + mean(sort(psi(a+1) - psi(b+1) - psi(c+1)))

@@ -49,6 +49,8 @@ def _declare(L):
         "ente_jitter_workspace_size": ([i32, i32], sz),
         "ente_jitter": ([vp, i32, cp, i32, u64p, dbl, vp, vp, sz, vp], i32),
         "ente_pack_te": ([vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32p, i32, vp, vp, vp], i32),
+        "ente_pack_te_items": ([vp, vp, i32, i32, i32, i32, i32, i32, i32, i32p, i32, vp, vp, vp],
+                               i32),
         "ente_te_reduce_workspace_size": ([cp, i32], sz),
         "ente_te_reduce": ([vp, i64, cp, i32, vp, i64, dbl, vp, vp, sz, vp], i32),
         "ente_launch_count": ([], i64),

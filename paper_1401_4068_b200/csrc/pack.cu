@@ -20,27 +20,29 @@ namespace ente {
 struct PackItem {
     int32_t u;
     int32_t perm;
+    int32_t t_lo;  // 1-based first sample of the item's window
+    int32_t pad_;
 };
 
 __global__ void __launch_bounds__(256) pack_te_kernel(
     const double *__restrict__ x, const double *__restrict__ y, int reps, int n_samples, int dx,
-    int tau_x, int dy, int tau_y, int t_lo, int w, const PackItem *__restrict__ items, int n_items,
+    int tau_x, int dy, int tau_y, int w, const PackItem *__restrict__ items, int n_items,
     const int32_t *__restrict__ perms, double *__restrict__ out) {
     const int64_t rows = (int64_t)reps * w;
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= rows) return;
-    for (int item = blockIdx.y; item < n_items; item += gridDim.y) {  // grid.y <= 65535
-    const PackItem it = items[item];
     const int r = (int)(row / w);
-    const int tp = t_lo + (int)(row - (int64_t)r * w);  // 1-based t'
-    const int ry = it.perm >= 0 ? perms[(int64_t)it.perm * reps + r] : r;
     const int dim = 1 + dy + dx;
-    double *o = out + ((int64_t)item * rows + row) * dim;
-    const double *yr = y + (int64_t)ry * n_samples;
-    const double *xr = x + (int64_t)r * n_samples;
-    o[0] = yr[tp - 1];
-    for (int j = 0; j < dy; ++j) o[1 + j] = yr[tp - 2 - j * tau_y];
-    for (int j = 0; j < dx; ++j) o[1 + dy + j] = xr[tp - 1 - it.u - j * tau_x];
+    for (int item = blockIdx.y; item < n_items; item += gridDim.y) {  // grid.y <= 65535
+        const PackItem it = items[item];
+        const int tp = it.t_lo + (int)(row - (int64_t)r * w);  // 1-based t'
+        const int ry = it.perm >= 0 ? perms[(int64_t)it.perm * reps + r] : r;
+        double *o = out + ((int64_t)item * rows + row) * dim;
+        const double *yr = y + (int64_t)ry * n_samples;
+        const double *xr = x + (int64_t)r * n_samples;
+        o[0] = yr[tp - 1];
+        for (int j = 0; j < dy; ++j) o[1 + j] = yr[tp - 2 - j * tau_y];
+        for (int j = 0; j < dx; ++j) o[1 + dy + j] = xr[tp - 1 - it.u - j * tau_x];
     }
 }
 
@@ -48,40 +50,62 @@ __global__ void __launch_bounds__(256) pack_te_kernel(
 
 using namespace ente;
 
+extern "C" int ente_pack_te_items(const double *x, const double *y, int reps, int n_samples,
+                                  int dx, int tau_x, int dy, int tau_y, int w,
+                                  const int32_t *items, int n_items, const int32_t *perms,
+                                  double *out, void *stream) {
+    if (n_items == 0) return ENTE_OK;
+    if (!x || !y || !out || !items || reps < 1 || n_samples < 1 || dx < 1 || dy < 1 || tau_x < 1 ||
+        tau_y < 1 || w < 1 || n_items < 0 || 1 + dx + dy > kMaxDim) {
+        set_error("ente_pack_te: bad arguments");
+        return ENTE_ERR_ARG;
+    }
+    std::vector<PackItem> h(n_items);
+    for (int i = 0; i < n_items; ++i) {
+        const int u = items[3 * i], perm = items[3 * i + 1], t_lo = items[3 * i + 2];
+        if (perm >= 0 && !perms) {
+            set_error("ente_pack_te: item %d needs a permutation table", i);
+            return ENTE_ERR_ARG;
+        }
+        // every sample read must exist (the host raises IndexUnderflow first)
+        if (u < 0 || t_lo - 1 - (dy - 1) * tau_y < 1 || t_lo - u - (dx - 1) * tau_x < 1 ||
+            t_lo + w - 1 > n_samples) {
+            set_error("ente_pack_te: item %d (u=%d, window start %d) outside the ensemble", i, u,
+                      t_lo);
+            return ENTE_ERR_ARG;
+        }
+        h[i] = PackItem{u, perm, t_lo, 0};
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // items travel as kernel-visible memory via a small stream-ordered copy
+    PackItem *ditems = nullptr;
+    ENTE_CUDA(cudaMallocAsync(&ditems, sizeof(PackItem) * n_items, st));
+    ENTE_CUDA(cudaMemcpyAsync(ditems, h.data(), sizeof(PackItem) * n_items, cudaMemcpyHostToDevice, st));
+    const int64_t rows = (int64_t)reps * w;
+    dim3 grid((unsigned)((rows + 255) / 256), (unsigned)(n_items < 65535 ? n_items : 65535));
+    ENTE_LAUNCH("pack_te", st,
+                pack_te_kernel<<<grid, 256, 0, st>>>(x, y, reps, n_samples, dx, tau_x, dy, tau_y, w,
+                                                     ditems, n_items, perms, out));
+    ENTE_CUDA(cudaGetLastError());
+    ENTE_CUDA(cudaFreeAsync(ditems, st));
+    // (a pageable-source cudaMemcpyAsync has staged h before returning)
+    return ENTE_OK;
+}
+
 extern "C" int ente_pack_te(const double *x, const double *y, int reps, int n_samples, int dx,
                             int tau_x, int dy, int tau_y, int t_lo, int t_hi, const int32_t *items,
                             int n_items, const int32_t *perms, double *out, void *stream) {
     if (n_items == 0) return ENTE_OK;
-    const int w = t_hi - t_lo + 1;
-    if (!x || !y || !out || !items || reps < 1 || n_samples < 1 || dx < 1 || dy < 1 || tau_x < 1 ||
-        tau_y < 1 || w < 1 || t_hi > n_samples || n_items < 0 || 1 + dx + dy > kMaxDim) {
+    if (!items || n_items < 0 || t_hi < t_lo) {
         set_error("ente_pack_te: bad arguments");
         return ENTE_ERR_ARG;
     }
-    // the earliest sample read must exist (IndexUnderflow is raised by the host)
-    int max_u = 0;
+    std::vector<int32_t> it3(3 * (size_t)n_items);
     for (int i = 0; i < n_items; ++i) {
-        if (items[2 * i + 1] >= 0 && !perms) {
-            set_error("ente_pack_te: item %d needs a permutation table", i);
-            return ENTE_ERR_ARG;
-        }
-        max_u = max_u > items[2 * i] ? max_u : items[2 * i];
+        it3[3 * i] = items[2 * i];
+        it3[3 * i + 1] = items[2 * i + 1];
+        it3[3 * i + 2] = t_lo;
     }
-    if (t_lo - 1 - (dy - 1) * tau_y < 1 || t_lo - max_u - (dx - 1) * tau_x < 1) {
-        set_error("ente_pack_te: window start %d underflows the embedding", t_lo);
-        return ENTE_ERR_ARG;
-    }
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // items travel as kernel-visible memory via a small device copy
-    PackItem *ditems = nullptr;
-    ENTE_CUDA(cudaMallocAsync(&ditems, sizeof(PackItem) * n_items, st));
-    ENTE_CUDA(cudaMemcpyAsync(ditems, items, sizeof(PackItem) * n_items, cudaMemcpyHostToDevice, st));
-    const int64_t rows = (int64_t)reps * w;
-    dim3 grid((unsigned)((rows + 255) / 256), (unsigned)(n_items < 65535 ? n_items : 65535));
-    ENTE_LAUNCH("pack_te", st,
-                pack_te_kernel<<<grid, 256, 0, st>>>(x, y, reps, n_samples, dx, tau_x, dy, tau_y,
-                                                     t_lo, w, ditems, n_items, perms, out));
-    ENTE_CUDA(cudaGetLastError());
-    ENTE_CUDA(cudaFreeAsync(ditems, st));
-    return ENTE_OK;
+    return ente_pack_te_items(x, y, reps, n_samples, dx, tau_x, dy, tau_y, t_hi - t_lo + 1,
+                              it3.data(), n_items, perms, out, stream);
 }

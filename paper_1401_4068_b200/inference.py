@@ -138,9 +138,11 @@ def jitter_state(seed_tuple) -> tuple:
 class PairPipeline:
     """Device pipeline for the chunks of one (source, target) pair.
 
-    run(items) takes (u, perm_index) items (perm_index -1 = original data)
-    and returns their TE values in order; errors are raised for the first
-    failing item, as the reference's per-u estimate_te_batch calls would.
+    run(items) takes (u, perm_index) items (perm_index -1 = original data),
+    or (u, perm_index, t_lo) items whose window starts at sample t_lo (all
+    windows config.window's width), and returns their TE values in order;
+    errors are raised for the first failing item, as the reference's per-u
+    estimate_te_batch calls would.
     """
 
     def __init__(self, source, target, spec_x, spec_y, config: AnalysisConfig):
@@ -179,17 +181,21 @@ class PairPipeline:
     def _wave(self, items) -> np.ndarray:
         L = nat.lib()
         n = len(items)
-        it = np.ascontiguousarray(np.array(items, dtype=np.int32).reshape(n, 2))
+        it = np.empty((n, 3), dtype=np.int32)
+        for i, item in enumerate(items):
+            it[i, 0], it[i, 1] = item[0], item[1]
+            it[i, 2] = item[2] if len(item) > 2 else self.t_lo
         pts = torch.empty((n * self.m, self.dim), dtype=torch.float64, device=self.x.device)
         perms_ptr = nat.ptr(self.perm_dev) if self.perm_dev is not None else None
-        nat.check(L.ente_pack_te(nat.ptr(self.x), nat.ptr(self.y), self.reps, self.n_samples,
-                                 self.sx.dim, self.sx.delay, self.sy.dim, self.sy.delay,
-                                 self.t_lo, self.t_hi,
-                                 it.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_int32)), n,
-                                 perms_ptr, nat.ptr(pts), nat.stream_handle()), "ente_pack_te")
+        nat.check(L.ente_pack_te_items(nat.ptr(self.x), nat.ptr(self.y), self.reps,
+                                       self.n_samples, self.sx.dim, self.sx.delay, self.sy.dim,
+                                       self.sy.delay, self.w,
+                                       it.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_int32)),
+                                       n, perms_ptr, nat.ptr(pts), nat.stream_handle()),
+                  "ente_pack_te_items")
         rows0 = np.arange(n, dtype=np.int64) * self.m
         ns = [self.m] * n
-        states = np.array([jitter_state(self.seed_tuple(u, p)) for u, p in items],
+        states = np.array([jitter_state(self.seed_tuple(item[0], item[1])) for item in items],
                           dtype=np.uint64)
         te, st = te_chunks_device(pts, rows0, ns, self.sy.dim, self.sx.dim, self.cfg.k,
                                   self.cfg.jitter_amplitude, states)
@@ -246,6 +252,72 @@ def analyze_pair(source: EnsembleSeries, target: EnsembleSeries,
                  for i in range(s)]
         pipe.set_perms(perms)
         te_surr = pipe.run([(u, i) for u in grid for i in range(s)]).reshape(len(grid), s)
+    surrogates = np.full(s, -np.inf)
+    for row in te_surr:
+        np.maximum(surrogates, row, out=surrogates)
+    p = permutation_pvalue(stat_orig, surrogates, config.conservative_pvalue)
+    sig = p < config.alpha
+    return TEResult(source=source.channel_name, target=target.channel_name,
+                    window=config.window, u_selected=u_best, te_value=te_best,
+                    surrogate_values=surrogates, p_value=p, significant=sig,
+                    significant_corrected=sig,
+                    te_minus_median_surrogate=te_best - float(np.median(surrogates)),
+                    te_curve=curve)
+
+
+def analyze_windows(source: EnsembleSeries, target: EnsembleSeries, spec_x: EmbeddingSpec,
+                    spec_y: EmbeddingSpec, config: AnalysisConfig, window_starts) -> list:
+    """analyze_pair for many windows of config.window's width in ONE device batch.
+
+    Equivalent to [analyze_pair(..., replace(config, window=(t, t + w - 1)))
+    for t in window_starts] (inference.py:120-193 per window; the seeds do not
+    depend on the window, so each window reuses the same permutations and
+    jitter streams, exactly as the per-window calls would).  This is the
+    non-stationary, TE-per-time-point analysis of the paper: every (window,
+    u, surrogate) chunk goes through one pack / jitter / search / reduce
+    sequence.
+    """
+    import dataclasses
+
+    validate_ensemble(source)
+    validate_ensemble(target)
+    if config.scan_statistic == "selected":
+        return [analyze_pair(source, target, spec_x, spec_y,
+                             dataclasses.replace(config, window=(t, t + _width(config) - 1)))
+                for t in window_starts]
+    w = _width(config)
+    grid = config.test_grid or config.u_candidates
+    us = list(config.u_candidates)
+    windows = [(int(t), int(t) + w - 1) for t in window_starts]
+    for lo, hi in windows:
+        for u in us:
+            check_assembly(source, target, spec_x, spec_y, u, (lo, hi))
+    pipe = PairPipeline(source, target, spec_x, spec_y, config)
+    reps, s = target.n_repetitions, config.n_surrogates
+    perms = [cached_permutation(config.seed, i, reps, config.strict_permutation) for i in range(s)]
+    pipe.set_perms(perms)
+    per_win = [(u, -1) for u in us] + [(u, i) for u in grid for i in range(s)]
+    items = [(u, i, lo) for lo, _ in windows for (u, i) in per_win]
+    te_all = pipe.run(items).reshape(len(windows), len(per_win))
+    results = []
+    for (lo, hi), row in zip(windows, te_all):
+        te_orig = row[:len(us)]
+        te_surr = row[len(us):].reshape(len(grid), s)
+        results.append(_assemble_result(source, target, dataclasses.replace(config, window=(lo, hi)),
+                                        us, grid, te_orig, te_surr))
+    return results
+
+
+def _width(config) -> int:
+    return config.window[1] - config.window[0] + 1
+
+
+def _assemble_result(source, target, config, us, grid, te_orig, te_surr) -> TEResult:
+    """Host statistics of analyze_pair (inference.py:153-193) for one window."""
+    s = config.n_surrogates
+    curve = [(u, float(t)) for u, t in zip(us, te_orig)]
+    u_best, te_best = max(curve, key=lambda ut: (ut[1], -ut[0]))
+    stat_orig = max(t for u, t in curve if u in grid)
     surrogates = np.full(s, -np.inf)
     for row in te_surr:
         np.maximum(surrogates, row, out=surrogates)

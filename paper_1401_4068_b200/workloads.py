@@ -149,9 +149,20 @@ class Workload:
     n_surrogates: int
     k: int = 4
     seed: int = 0
+    window_starts: tuple = None  # many windows of window's width (TE per time point)
+    n_pairs: int = 1             # channel pairs (pair p uses ensembles(p))
 
-    def ensembles(self):
-        return _ENSEMBLES[self.name]()
+    def ensembles(self, pair: int = 0):
+        return _ENSEMBLES[self.name](pair)
+
+    def items(self, n_surrogates=None):
+        """(u, perm_index[, t_lo]) chunk items of one pair: analyze_pair's order."""
+        s = self.n_surrogates if n_surrogates is None else n_surrogates
+        per = [(u, -1) for u in self.u_candidates] + [(u, i) for u in self.u_candidates
+                                                      for i in range(s)]
+        if self.window_starts is None:
+            return per
+        return [(u, i, t) for t in self.window_starts for (u, i) in per]
 
     @property
     def chunk_points(self) -> int:
@@ -159,10 +170,10 @@ class Workload:
 
 
 _ENSEMBLES = {
-    "C1": lambda: ar_pair("unidirectional", 50, 3000, seed=0),
-    "C2": lambda: lorenz_pair(5, 500, 200, gamma_schedule=lambda t: 0.3, seed=0),
-    "C4": lambda: ar_pair("unidirectional", 500, 1600, seed=0),
-    "C5": lambda: ar_pair("bidirectional", 250, 1000, seed=0),
+    "C1": lambda p: ar_pair("unidirectional", 50, 3000, seed=p),
+    "C2": lambda p: lorenz_pair(5, 500, 200, gamma_schedule=lambda t: 0.3, seed=p),
+    "C4": lambda p: ar_pair("unidirectional", 500, 1600, seed=p),
+    "C5": lambda p: ar_pair("bidirectional", 250, 1000, seed=p),
 }
 
 CONFIGS = {
@@ -170,8 +181,10 @@ CONFIGS = {
                          "window (1101,1400), S=500", (2, 1), (1,), (1101, 1400), 500),
     "C2": Workload("C2", "coupled Lorenz, 500 trials, dim=3, tau=1, u=1..10, k=4, "
                          "window (121,180), S=200", (3, 1), tuple(range(1, 11)), (121, 180), 200),
-    "C4": Workload("C4", "AR(1) per time point, 500 trials, dim=2, u=10, window (t,t), S=200",
-                   (2, 1), (10,), (501, 501), 200),
-    "C5": Workload("C5", "MEG-shaped AR bidirectional, 250 trials, dim=3, u=5..17 step 2, "
-                         "window (801,890), S=500", (3, 1), tuple(range(5, 18, 2)), (801, 890), 500),
+    "C4": Workload("C4", "non-stationary AR(1): TE per time point t=501..1500 (window (t,t)), "
+                         "500 trials, dim=2, u=10, S=200", (2, 1), (10,), (501, 501), 200,
+                   window_starts=tuple(range(501, 1501))),
+    "C5": Workload("C5", "MEG-shaped AR bidirectional: 20 channel pairs x 250 trials, dim=3, "
+                         "u=5..17 step 2, window (801,890), S=500", (3, 1), tuple(range(5, 18, 2)),
+                   (801, 890), 500, n_pairs=20),
 }

@@ -140,3 +140,29 @@ def test_config_chunks_match_reference(golden, name, key, u, idx):
         pipe.set_perms(perms)
     te = pipe.run([(u, -1 if i is None else i) for i in idx])
     assert np.array_equal(te, g[key])
+
+
+def test_analyze_windows_equals_per_window_analyze_pair():
+    """One device batch over many windows == one analyze_pair call per window."""
+    import dataclasses
+    from paper_1401_4068_b200 import analyze_windows
+    wl = workloads.CONFIGS["C4"]
+    xv, yv = wl.ensembles()
+    xv, yv = xv[:60], yv[:60]  # 60 trials keep the per-window calls quick
+    spec = EmbeddingSpec(*wl.spec)
+    cfg = AnalysisConfig(u_candidates=(8, 10), window=(501, 501), k=4, n_surrogates=20, seed=3)
+    X, Y = EnsembleSeries("X", xv), EnsembleSeries("Y", yv)
+    starts = [501, 777, 1200]
+    batch = analyze_windows(X, Y, spec, spec, cfg, starts)
+    for t, res in zip(starts, batch):
+        one = analyze_pair(X, Y, spec, spec, dataclasses.replace(cfg, window=(t, t)))
+        assert res.window == one.window == (t, t)
+        assert res.te_curve == one.te_curve
+        assert res.surrogate_values.tolist() == one.surrogate_values.tolist()
+        assert (res.u_selected, res.te_value, res.p_value) == (one.u_selected, one.te_value,
+                                                               one.p_value)
+    # and the batch agrees with the CPU oracle's analyze_pair on one window
+    ref = oracle.analyze_pair(xv, yv, wl.spec, wl.spec, (8, 10), (777, 777), k=4,
+                              n_surrogates=20, seed=3)
+    assert batch[1].te_value == ref["te_value"]
+    assert batch[1].surrogate_values.tolist() == list(ref["surrogate_values"])
