@@ -268,9 +268,14 @@ def run_ours(args):
     value = n_chunks * world / (ms * 1e-3)
 
     # roofline of the dominant kernel (FP32 CUDA-core bound)
-    pce_pass = n_chunks * m * (m - 1) * dim  # per launch: one pass over all ordered pairs
+    # algorithmic work of one sweep over a step's chunks (all ordered pairs x columns);
+    # a step may launch each sweep several times (one per pair / wave): per-launch
+    # figures are the per-step ones divided by the launches per step
+    pce_step = n_chunks * m * (m - 1) * dim
     dom = max((k for k in prof if k in ("knn_pass", "count_pass")), key=lambda k: prof[k]["ms"])
+    launches_per_step = max(1, prof[dom]["launches"]) / args.steps
     per_launch_ms = prof[dom]["ms"] / max(1, prof[dom]["launches"])
+    pce_pass = pce_step / launches_per_step  # per launch
     achieved = 2.0 * pce_pass / (per_launch_ms * 1e-3) / 1e12
     props = torch.cuda.get_device_properties(local)
     peaks = {}

@@ -99,12 +99,15 @@ def stream_handle() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+_CHUNK_DTYPE = np.dtype([("row0", "<i8"), ("n", "<i4"), ("reserved", "<i4")])
+
+
 def chunk_table(rows0, ns):
-    arr = (ChunkDesc * len(ns))()
-    for i, (r, n) in enumerate(zip(rows0, ns)):
-        arr[i].row0 = int(r)
-        arr[i].n = int(n)
-    return arr
+    """ente_chunk[] for the C ABI (vectorised; the pointer keeps the array alive)."""
+    arr = np.zeros(len(ns), dtype=_CHUNK_DTYPE)
+    arr["row0"] = np.asarray(rows0, dtype=np.int64)
+    arr["n"] = np.asarray(ns, dtype=np.int32)
+    return arr.ctypes.data_as(ctypes.POINTER(ChunkDesc))
 
 
 def ptr(t: torch.Tensor) -> int:

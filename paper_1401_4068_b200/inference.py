@@ -167,24 +167,36 @@ class PairPipeline:
     def seed_tuple(self, u, perm_index):
         return (self.cfg.seed, u, 0 if perm_index < 0 else perm_index + 1)
 
+    def _items(self, items) -> np.ndarray:
+        it = np.asarray(items, dtype=np.int64)
+        if it.ndim != 2 or it.shape[1] not in (2, 3):
+            raise ValueError("items must be (u, perm_index) or (u, perm_index, t_lo) tuples")
+        if it.shape[1] == 2:
+            it = np.concatenate([it, np.full((len(it), 1), self.t_lo, dtype=np.int64)], axis=1)
+        return np.ascontiguousarray(it.astype(np.int32))
+
     def run(self, items) -> np.ndarray:
-        if not items:
+        if len(items) == 0:
             return np.empty(0)
         if self.m <= self.cfg.k:
             raise KTooLarge(f"need more than k={self.cfg.k} pooled points, got {self.m}")
+        it = self._items(items)
         per_wave = max(1, MAX_ROWS_PER_WAVE // self.m)
         out = []
-        for s in range(0, len(items), per_wave):
-            out.append(self._wave(items[s:s + per_wave]))
+        for s in range(0, len(it), per_wave):
+            out.append(self._wave(it[s:s + per_wave]))
         return np.concatenate(out)
 
-    def _wave(self, items) -> np.ndarray:
+    def _states(self, it: np.ndarray) -> np.ndarray:
+        """Jitter PCG64 states per item; seeds depend only on (u, perm), not the window."""
+        keys, inv = np.unique(it[:, :2], axis=0, return_inverse=True)
+        uniq = np.array([jitter_state(self.seed_tuple(int(u), int(p))) for u, p in keys],
+                        dtype=np.uint64)
+        return np.ascontiguousarray(uniq[inv.reshape(-1)])
+
+    def _wave(self, it: np.ndarray) -> np.ndarray:
         L = nat.lib()
-        n = len(items)
-        it = np.empty((n, 3), dtype=np.int32)
-        for i, item in enumerate(items):
-            it[i, 0], it[i, 1] = item[0], item[1]
-            it[i, 2] = item[2] if len(item) > 2 else self.t_lo
+        n = len(it)
         pts = torch.empty((n * self.m, self.dim), dtype=torch.float64, device=self.x.device)
         perms_ptr = nat.ptr(self.perm_dev) if self.perm_dev is not None else None
         nat.check(L.ente_pack_te_items(nat.ptr(self.x), nat.ptr(self.y), self.reps,
@@ -194,11 +206,9 @@ class PairPipeline:
                                        n, perms_ptr, nat.ptr(pts), nat.stream_handle()),
                   "ente_pack_te_items")
         rows0 = np.arange(n, dtype=np.int64) * self.m
-        ns = [self.m] * n
-        states = np.array([jitter_state(self.seed_tuple(item[0], item[1])) for item in items],
-                          dtype=np.uint64)
+        ns = np.full(n, self.m, dtype=np.int64)
         te, st = te_chunks_device(pts, rows0, ns, self.sy.dim, self.sx.dim, self.cfg.k,
-                                  self.cfg.jitter_amplitude, states)
+                                  self.cfg.jitter_amplitude, self._states(it))
         if te is None:
             _raise_status(int(st[np.flatnonzero(st)[0]]))
         return te.cpu().numpy()

@@ -63,7 +63,7 @@ def te_reduce_device(counts: torch.Tensor, rows0, ns, k: int) -> torch.Tensor:
     """ente_te_reduce over a [3, rows] int32 device count matrix; returns [n_chunks] f64."""
     L = nat.lib()
     rows = counts.shape[1]
-    psi = _PSI.get(int(max(ns)) + 2)
+    psi = _PSI.get(int(np.max(ns)) + 2)
     out = torch.empty(len(ns), dtype=torch.float64, device=counts.device)
     table = nat.chunk_table(rows0, ns)
     ws = nat.workspace(L.ente_te_reduce_workspace_size(table, len(ns)))
