@@ -130,6 +130,39 @@ def workspace(nbytes: int) -> torch.Tensor:
     return buf
 
 
+class _Scratch(threading.local):
+    bufs = None
+
+
+_scratch = _Scratch()
+
+
+def scratch(name: str, shape, dtype: torch.dtype) -> torch.Tensor:
+    """A named, grow-only, per-thread device buffer viewed as `shape` of `dtype`.
+
+    The pipeline's big per-wave arrays (packed joints, eps, counts) live here
+    so that repeated waves reuse the same resident HBM instead of going
+    through the caching allocator (whose splits of multi-GB blocks ended in
+    fresh cudaMalloc + first-touch costs of hundreds of ms per call).  The
+    contents are overwritten by the next call that uses the same name, so
+    callers copy results out before returning them.
+    """
+    if _scratch.bufs is None:
+        _scratch.bufs = {}
+    numel = 1
+    for s in shape:
+        numel *= int(s)
+    nbytes = max(1, numel * torch.empty((), dtype=dtype).element_size())
+    dev = device()
+    buf = _scratch.bufs.get(name)
+    if buf is None or buf.numel() < nbytes or buf.device != dev:
+        _scratch.bufs[name] = None
+        del buf
+        buf = torch.empty(nbytes + (nbytes >> 4), dtype=torch.uint8, device=dev)
+        _scratch.bufs[name] = buf
+    return buf[:nbytes].view(dtype).view(tuple(int(s) for s in shape))
+
+
 def masks_array(masks):
     arr = (ctypes.c_uint32 * max(1, len(masks)))()
     for i, m in enumerate(masks):

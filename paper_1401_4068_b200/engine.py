@@ -79,11 +79,12 @@ def column_mask(cols, dim: int) -> int:
 # ---------------------------------------------------------------------------
 # device-level entry points (tensors in, tensors out; used by ksg / bench)
 # ---------------------------------------------------------------------------
-def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int):
+def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int, reuse: bool = False):
     """ente_search on a device-resident [rows, dim] fp64 matrix.
 
     Returns (eps [rows] f64, counts [n_marg, rows] int32, status [n_chunks] int32),
-    all on the device, stream-ordered on the current stream.
+    all on the device, stream-ordered on the current stream.  With reuse the
+    outputs live in the named scratch pool (valid until the next reuse call).
     """
     if pts64.dtype != torch.float64 or not pts64.is_cuda or not pts64.is_contiguous():
         raise TypeError("pts64 must be a contiguous CUDA float64 tensor")
@@ -91,9 +92,14 @@ def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int):
     L = nat.lib()
     table = nat.chunk_table(rows0, ns)
     marr = nat.masks_array(masks)
-    eps = torch.empty(rows, dtype=torch.float64, device=pts64.device)
-    counts = torch.empty((max(1, len(masks)), rows), dtype=torch.int32, device=pts64.device)
-    status = torch.empty(max(1, len(ns)), dtype=torch.int32, device=pts64.device)
+    if reuse:
+        eps = nat.scratch("search.eps", (rows,), torch.float64)
+        counts = nat.scratch("search.counts", (max(1, len(masks)), rows), torch.int32)
+        status = nat.scratch("search.status", (max(1, len(ns)),), torch.int32)
+    else:
+        eps = torch.empty(rows, dtype=torch.float64, device=pts64.device)
+        counts = torch.empty((max(1, len(masks)), rows), dtype=torch.int32, device=pts64.device)
+        status = torch.empty(max(1, len(ns)), dtype=torch.int32, device=pts64.device)
     need = L.ente_search_workspace_size(table, len(ns), dim, len(masks), int(k))
     ws = nat.workspace(need)
     nat.check(L.ente_search(nat.ptr(pts64), rows, dim, table, len(ns), marr, len(masks), int(k),

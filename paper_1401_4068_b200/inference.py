@@ -197,7 +197,7 @@ class PairPipeline:
     def _wave(self, it: np.ndarray) -> np.ndarray:
         L = nat.lib()
         n = len(it)
-        pts = torch.empty((n * self.m, self.dim), dtype=torch.float64, device=self.x.device)
+        pts = nat.scratch("pipe.joint", (n * self.m, self.dim), torch.float64)
         perms_ptr = nat.ptr(self.perm_dev) if self.perm_dev is not None else None
         nat.check(L.ente_pack_te_items(nat.ptr(self.x), nat.ptr(self.y), self.reps,
                                        self.n_samples, self.sx.dim, self.sx.delay, self.sy.dim,

@@ -125,7 +125,7 @@ def te_chunks_device(pts64: torch.Tensor, rows0, ns, d_y: int, d_x: int, k: int,
     st = status.cpu().numpy()
     if (st != 0).any():
         return None, st
-    _, counts, sstatus = search_device(pts64, rows0, ns, te_masks(d_y, d_x), k)
+    _, counts, sstatus = search_device(pts64, rows0, ns, te_masks(d_y, d_x), k, reuse=True)
     te = te_reduce_device(counts, rows0, ns, k)
     return te, st
 
