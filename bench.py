@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--surrogates", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shape", default="30094,17,64,bench",
+                    help="C3 cell: n,dim,chunks,layout[,tied] (layout te|bench|knn)")
     return ap.parse_args()
 
 
@@ -186,6 +188,226 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+
+# ---------------------------------------------------------------------------
+# roofline of the dominant sweep (FP32 CUDA-core / issue bound)
+# ---------------------------------------------------------------------------
+def roofline_of(prof, steps, pce_step, knn_sub, cnt_sub, dim, local):
+    """roofline JSON object of the dominant sweep kernel.
+
+    pce_step: algorithmic pair-coordinate evaluations per step for each
+    sweep (ordered pairs x the columns the pass must compare); a step may
+    launch a sweep several times (one per pair / wave), so per-launch
+    figures are the per-step ones divided by the launches per step.
+    """
+    import torch
+    from paper_1401_4068_b200 import _native as nat
+    dom = max((k for k in prof if k in ("knn_pass", "count_pass")), key=lambda k: prof[k]["ms"])
+    launches_per_step = max(1, prof[dom]["launches"]) / steps
+    per_launch_ms = prof[dom]["ms"] / max(1, prof[dom]["launches"])
+    pce_pass = pce_step[dom] / launches_per_step  # per launch
+    achieved = 2.0 * pce_pass / (per_launch_ms * 1e-3) / 1e12
+    props = torch.cuda.get_device_properties(local)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    nominal = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
+    measured_loop = 2.0 * nat.microbench_pce(100) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    total_ms = sum(v["ms"] for v in prof.values())
+    # pruned work actually evaluated: sub-tiles of 32 candidates x 128 references
+    sub_pce = 32 * 128 * dim
+    evaluated = {k: n * sub_pce / max(1, prof.get(k, {}).get("launches", 1))
+                 for k, n in (("knn_pass", knn_sub), ("count_pass", cnt_sub))}
+    ev_rate = 2.0 * evaluated[dom] / (per_launch_ms * 1e-3) / 1e12
+    return {"bound": "fp32", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
+            "frac": achieved / nominal, "traffic": traffic, "kernel": dom,
+            "peak_kind": f"nominal: {props.multi_processor_count} SMs x 128 lanes x 2 ops x "
+                         f"{sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz); FP32 peak is not in "
+                         "MEASURED_PEAKS.json",
+            "measured_loop_peak": measured_loop,
+            "frac_of_measured_loop": achieved / measured_loop,
+            "kernel_share_of_step": prof[dom]["ms"] / total_ms if total_ms else None,
+            "kernels_ms_per_step": {k: v["ms"] / steps for k, v in prof.items()},
+            "pce_per_launch": pce_pass,
+            "evaluated_pce_per_launch": evaluated,
+            "evaluated_fraction": {k: v / (pce_step[k] / launches_per_step)
+                                   for k, v in evaluated.items()},
+            "evaluated_tflops": ev_rate,
+            "evaluated_frac": ev_rate / nominal,
+            "work_definition": "ordered pairs x columns compared by the pass (kNN: all D; "
+                               "counts: the union of the marginal columns; SURVEY 8d), "
+                               "2 FP32 ops per pair-coordinate"}
+
+
+# ---------------------------------------------------------------------------
+# C3: kNN + range-search sweep cell (searches/s)
+# ---------------------------------------------------------------------------
+def c3_cell(args):
+    parts = args.shape.split(",")
+    n, dim, chunks, layout = int(parts[0]), int(parts[1]), int(parts[2]), parts[3]
+    tied = len(parts) > 4 and parts[4] == "tied"
+    return n, dim, chunks, layout, tied
+
+
+def c3_cpu_sample(n, dim, layout, tied, k, budget_s=12.0, max_chunks=8):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    from paper_1401_4068_b200 import workloads
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    margs = workloads.c3_marginals(dim, layout)
+    done, t0 = 0, time.perf_counter()
+    while done < max_chunks and (done < 1 or time.perf_counter() - t0 < budget_s):
+        oracle.search(workloads.c3_chunk(n, dim, done, tied), margs, k)
+        done += 1
+    dt = time.perf_counter() - t0
+    return {"value": done * n / dt, "unit": "searches/s", "cores": cores, "kind": "port",
+            "sample": f"{done} chunk(s) of the C3 cell n={n} dim={dim} layout={layout}"
+                      f"{' tied' if tied else ''}, {dt:.1f} s; C oracle (oracle/ente_oracle.c) "
+                      "restating the reference sorted sweep engine.py:70-160, OpenMP"}
+
+
+def c3_config(n, dim, chunks, layout, tied, k, world):
+    return {"workload": f"C3: kNN+range-search sweep cell, {chunks} chunks x {n} points, "
+                        f"dim={dim}, layout={layout}{' (tied)' if tied else ''}, k={k}",
+            "chunks_per_step": chunks, "points_per_chunk": n, "dim": dim, "layout": layout,
+            "k": k, "parallelism": f"dp{world} (chunk sharding)",
+            "l2": f"{'inputs larger than L2' if chunks * n * dim * 8 > 126e6 else 'inputs smaller than L2: L2 flushed between steps'}: "
+                  f"{chunks * n * dim * 8 / 1e9:.2f} GB of fp64 chunks per step"}
+
+
+def run_c3_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    n, dim, chunks, layout, tied = c3_cell(args)
+    for _ in range(args.warmup):
+        c3_cpu_sample(n, dim, layout, tied, 4, budget_s=0.0, max_chunks=1)
+    t0 = time.perf_counter()
+    samples = [c3_cpu_sample(n, dim, layout, tied, 4, budget_s=5.0, max_chunks=4)
+               for _ in range(args.steps)]
+    dt = time.perf_counter() - t0
+    rate = statistics.median([smp["value"] for smp in samples])
+    line = {"impl": "reference", "metric": "kNN+range searches/sec", "value": rate,
+            "unit": "searches/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY 8d C3 generator)",
+            "config": c3_config(n, dim, chunks, layout, tied, 4, args.gpus),
+            "cpu_baseline": {**samples[-1], "value": rate},
+            "e2e": {"value": rate, "unit": "searches/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_c3(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1401_4068_b200 import _native as nat, workloads
+    from paper_1401_4068_b200.engine import Chunk, batch_search, column_mask, search_device
+    n, dim, chunks, layout, tied = c3_cell(args)
+    k = 4
+    margs = workloads.c3_marginals(dim, layout)
+    masks = [column_mask(c, dim) for c in margs]
+    # weak scaling: rank r searches chunks [r*chunks, (r+1)*chunks) of the cell
+    host = [workloads.c3_chunk(n, dim, rank * chunks + c, tied) for c in range(chunks)]
+    pts = torch.from_numpy(np.concatenate(host)).cuda()
+    rows0 = np.arange(chunks, dtype=np.int64) * n
+    ns = np.full(chunks, n, dtype=np.int64)
+    flush = None
+    if chunks * n * dim * 8 < 2 * 126e6:  # small cell: flush L2 between steps
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        if flush is not None:
+            flush.zero_()
+        search_device(pts, rows0, ns, masks, k, reuse=True)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    clk = ClockSampler(local).__enter__()
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    nat.search_work()
+    launches0 = nat.launch_count()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    with nat.KernelProfile():
+        t_abs = time.time()
+        start.record()
+        for _ in range(args.steps):
+            step()
+        stop.record()
+        barrier()
+        clk.mark(t_abs, time.time())
+        prof = nat.KernelProfile.read()
+    launches = nat.launch_count() - launches0
+    knn_sub, cnt_sub = nat.search_work()
+    clk.__exit__(None, None, None)
+    ms = start.elapsed_time(stop) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = chunks * n * world / (ms * 1e-3)
+    union = len(set(c for cols in margs for c in cols))
+    pairs = chunks * n * (n - 1)
+    roofline = roofline_of(prof, args.steps, {"knn_pass": pairs * dim, "count_pass": pairs * union},
+                           knn_sub, cnt_sub, dim, local)
+
+    e2e = None
+    if not args.no_e2e:
+        items = [(Chunk(p, chunk_id=i), margs) for i, p in enumerate(host)]
+        batch_search(items[:1], k)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res = batch_search(items, k)
+        barrier()
+        e_s = (time.perf_counter() - t0) / args.steps
+        assert not any(isinstance(r, Exception) for r in res)
+        if dist is not None:
+            t = torch.tensor([e_s], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_s = float(t.item())
+        e2e = {"value": chunks * n * world / e_s, "unit": "searches/s",
+               "h2d_bytes_per_step": chunks * n * dim * 8,
+               "d2h_bytes_per_step": chunks * n * (8 + 4 * len(masks)) + 4 * chunks,
+               "api": "paper_1401_4068_b200.batch_search"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = c3_cpu_sample(n, dim, layout, tied, k)
+    if rank == 0:
+        line = {"metric": "kNN+range searches/sec", "value": value, "unit": "searches/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32+f64", "data": "synthetic (SURVEY 8d C3 generator)",
+                "config": c3_config(n, dim, chunks, layout, tied, k, world),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": clk.summary(), "gpu_launches": launches}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -267,51 +489,11 @@ def run_ours(args):
         ms = float(t.item())
     value = n_chunks * world / (ms * 1e-3)
 
-    # roofline of the dominant kernel (FP32 CUDA-core bound)
-    # algorithmic work of one sweep over a step's chunks (all ordered pairs x columns);
-    # a step may launch each sweep several times (one per pair / wave): per-launch
-    # figures are the per-step ones divided by the launches per step
+    # roofline of the dominant kernel (FP32 CUDA-core bound): algorithmic work
+    # of one pass over a step's chunks = all ordered pairs x columns
     pce_step = n_chunks * m * (m - 1) * dim
-    dom = max((k for k in prof if k in ("knn_pass", "count_pass")), key=lambda k: prof[k]["ms"])
-    launches_per_step = max(1, prof[dom]["launches"]) / args.steps
-    per_launch_ms = prof[dom]["ms"] / max(1, prof[dom]["launches"])
-    pce_pass = pce_step / launches_per_step  # per launch
-    achieved = 2.0 * pce_pass / (per_launch_ms * 1e-3) / 1e12
-    props = torch.cuda.get_device_properties(local)
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    nominal = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
-    measured_loop = 2.0 * nat.microbench_pce(100) / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(dom)
-    total_ms = sum(v["ms"] for v in prof.values())
-    # pruned work actually evaluated: sub-tiles of 32 candidates x 128 references
-    sub_pce = 32 * 128 * dim
-    evaluated = {k: n * sub_pce / max(1, prof.get(k, {}).get("launches", 1))
-                 for k, n in (("knn_pass", knn_sub), ("count_pass", cnt_sub))}
-    ev_rate = 2.0 * evaluated[dom] / (per_launch_ms * 1e-3) / 1e12
-    roofline = {"bound": "fp32", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
-                "frac": achieved / nominal, "traffic": traffic, "kernel": dom,
-                "peak_kind": f"nominal: {props.multi_processor_count} SMs x 128 lanes x 2 ops x "
-                             f"{sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz); FP32 peak is not in "
-                             "MEASURED_PEAKS.json",
-                "measured_loop_peak": measured_loop,
-                "frac_of_measured_loop": achieved / measured_loop,
-                "kernel_share_of_step": prof[dom]["ms"] / total_ms if total_ms else None,
-                "kernels_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
-                "pce_per_launch": pce_pass,
-                "evaluated_pce_per_launch": evaluated,
-                "evaluated_fraction": {k: v / pce_pass for k, v in evaluated.items()},
-                "evaluated_tflops": ev_rate,
-                "evaluated_frac": ev_rate / nominal,
-                "work_definition": "ordered pairs x columns (n(n-1)D per pass, 2 passes; "
-                                   "SURVEY 8d), 2 FP32 ops per pair-coordinate"}
+    roofline = roofline_of(prof, args.steps, {"knn_pass": pce_step, "count_pass": pce_step},
+                           knn_sub, cnt_sub, dim, local)
 
     # end-to-end through the public API (host ensembles, H2D + D2H in the region)
     e2e = None
@@ -369,7 +551,9 @@ def run_ours(args):
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.config == "C3":
+        run_c3_reference(args) if args.impl == "reference" else run_c3(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -16,7 +16,8 @@ import numpy as np
 import torch
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libente_b200.so")
+# ENTE_LIB overrides the library path (development A/B builds only)
+LIB_PATH = os.environ.get("ENTE_LIB") or os.path.join(PKG_DIR, "libente_b200.so")
 
 CHUNK_OK, CHUNK_K_TOO_LARGE, CHUNK_NONFINITE, CHUNK_DEGENERATE = 0, 1, 2, 3
 

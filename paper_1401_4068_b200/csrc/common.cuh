@@ -16,7 +16,10 @@ namespace ente {
 constexpr int kMaxDim = 32;     // column bitmasks are uint32
 constexpr int kMaxMarg = 8;     // marginals per search call
 constexpr int kNT = 128;        // threads per CTA in the sweep kernels
-constexpr int kRT = 4;          // reference points per thread
+#ifndef ENTE_KRT
+#define ENTE_KRT 2
+#endif
+constexpr int kRT = ENTE_KRT;   // reference points per thread (sweep lanes)
 constexpr int kRefTile = kNT * kRT;
 constexpr int kTJ = 128;        // candidate points per shared-memory stage
 constexpr int kCap = 16;        // band events kept per reference point

@@ -218,6 +218,24 @@ __global__ void __launch_bounds__(kTJ) gather_kernel(const double *__restrict__ 
 }
 
 // ---------------------------------------------------------------------------
+// sweep tile t -> (chunk, first sorted reference): tile0[c] = first tile of
+// chunk c (ascending, n_chunks + 1 entries); chunks without tiles repeat
+// their successor's value, so the largest c with tile0[c] <= t is the owner
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ TileRef tile_of(const int32_t *__restrict__ tile0, int n_chunks, int t) {
+    int lo = 0, hi = n_chunks - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(tile0 + mid) <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    TileRef tr;
+    tr.chunk = lo;
+    tr.r0 = (t - __ldg(tile0 + lo)) * kWarpRefs;
+    return tr;
+}
+
+// ---------------------------------------------------------------------------
 // register-level helpers for the fp32 sweeps
 // TE layout columns: 0 = y_t, 1..DY = y-past, DY+1..D-1 = x-past
 // (embedding.py:50-60).  Coordinates are held as packed pairs (0,1), (2,3)...
@@ -437,12 +455,12 @@ __device__ __forceinline__ void ring_issue(Ring<DP, NSLOT> &ring, int slot, cons
 template <int DY, int DX, int S>
 __global__ void __launch_bounds__(32) knn_pass_kernel(
     const float *__restrict__ pts32, const float *__restrict__ fbox,
-    const ChunkInfo *__restrict__ info, const TileRef *__restrict__ tiles, int k, int prune,
+    const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks, int k, int prune,
     float *__restrict__ t32_out, int32_t *__restrict__ L_out, unsigned long long *__restrict__ work) {
     using L = Lay<DY, DX>;
     constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG, NSLOT = L::NSLOT;
     __shared__ __align__(128) Ring<DP, NSLOT> ring;
-    const TileRef tr = tiles[blockIdx.x];
+    const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
     const int lane = threadIdx.x;
@@ -562,14 +580,14 @@ __global__ void __launch_bounds__(32) knn_pass_kernel(
 template <int DY, int DX>
 __global__ void __launch_bounds__(32) count_pass_kernel(
     const float *__restrict__ pts32, const float *__restrict__ fbox,
-    const ChunkInfo *__restrict__ info, const TileRef *__restrict__ tiles,
+    const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks,
     const float *__restrict__ t32_in, int64_t ws_rows, int prune, int32_t *__restrict__ cnt_out,
     uint32_t *__restrict__ ev, int32_t *__restrict__ ev_n, uint32_t fmask,
     unsigned long long *__restrict__ work) {
     using L = Lay<DY, DX>;
     constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG, NSLOT = L::NSLOT;
     __shared__ __align__(128) Ring<DP, NSLOT> ring;
-    const TileRef tr = tiles[blockIdx.x];
+    const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
     const int lane = threadIdx.x;
@@ -741,12 +759,13 @@ __device__ __forceinline__ void te_dist64(const double *ref, const double *q, in
 
 __global__ void __launch_bounds__(kWarpRefs) resolve_kernel(
     const double *__restrict__ pts64, int dim, const ChunkInfo *__restrict__ info,
-    const TileRef *__restrict__ tiles, int k, TeLayout lay, const int32_t *__restrict__ perm,
+    const int32_t *__restrict__ tile0, int n_chunks, int k, TeLayout lay, const int32_t *__restrict__ perm,
     const int32_t *__restrict__ L_in, const int32_t *__restrict__ cnt_in,
     const uint32_t *__restrict__ ev, const int32_t *__restrict__ ev_n, int64_t ws_rows,
     int64_t total_rows, double *__restrict__ out_eps, int32_t *__restrict__ out_counts,
-    int64_t *__restrict__ ovf_list, int32_t *__restrict__ ovf_n) {
-    const TileRef tr = tiles[blockIdx.x];
+    int64_t *__restrict__ ovf_list, int32_t *__restrict__ ovf_n, int64_t *__restrict__ rs_list,
+    int32_t *__restrict__ rs_n) {
+    const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     const int s = tr.r0 + threadIdx.x;  // sorted position
     if (s >= ci.n) return;
@@ -794,8 +813,13 @@ __global__ void __launch_bounds__(kWarpRefs) resolve_kernel(
         }
     }
     if (fallback) {
-        const int slot = atomicAdd(ovf_n, 1);
-        ovf_list[slot] = row;
+        if (ci.ok32) {  // fp32 data usable: pruned warp rescan of the sorted row
+            const int slot = atomicAdd(rs_n, 1);
+            rs_list[slot] = srow;
+        } else {
+            const int slot = atomicAdd(ovf_n, 1);
+            ovf_list[slot] = row;
+        }
         return;
     }
     out_eps[row] = eps;
@@ -805,6 +829,152 @@ __global__ void __launch_bounds__(kWarpRefs) resolve_kernel(
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// rescan: exact eps and counts for references whose band events overflowed
+// (heavily tied data).  One warp per listed sorted row; the lanes take the
+// 32 candidates of a sub-tile, sub-tiles are pruned by their gate boxes, and
+// every candidate the fp32 filter cannot decide is settled in fp64 on the
+// spot, so there is no per-point event limit:
+//   A  eps = k-th smallest joint d64 over the candidates with d32 <= hiA,
+//      hiA = up(t32 + 2 delta) (they include the true k nearest); per-lane
+//      sorted fp64 lists, k rounds of warp-minimum extraction
+//   B  with eps exact: v32 < lo = down(eps - delta) -> inside,
+//      v32 > hi = up(eps + delta) -> outside, otherwise compare v64 < eps
+// ---------------------------------------------------------------------------
+constexpr int kRescanWarps = 4;
+
+template <int DY, int DX, int S>
+__global__ void __launch_bounds__(kRescanWarps * 32) rescan_kernel(
+    const float *__restrict__ pts32, const float *__restrict__ fbox, const double *__restrict__ pts64,
+    const ChunkInfo *__restrict__ info, int n_chunks, const int32_t *__restrict__ perm,
+    const float *__restrict__ t32_in, const int64_t *__restrict__ list,
+    const int32_t *__restrict__ list_n, int k, TeLayout lay, int64_t total_rows,
+    double *__restrict__ out_eps, int32_t *__restrict__ out_counts) {
+    using L = Lay<DY, DX>;
+    constexpr int D = L::D, DP = L::DP, NP = L::NP;
+    constexpr int NG = DY < kGate ? DY : kGate;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * kRescanWarps;
+    const int64_t count = *list_n;
+    for (int64_t it = (int64_t)blockIdx.x * kRescanWarps + (threadIdx.x >> 5); it < count;
+         it += nwarps) {
+        const int64_t srow = list[it];
+        const int c = chunk_of_row(info, n_chunks, srow);
+        const ChunkInfo ci = info[c];
+        const int s = (int)(srow - ci.row0);  // sorted position of the reference
+        const int64_t row = ci.row0 + perm[srow];
+        const float *cp = pts32 + ci.prow0 * DP;
+        const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2;
+        const int nsub = ci.npad / kSub;
+        float2 ref[NP];
+        load_ref<D>(ref, cp + (int64_t)s * DP, true);
+        double r64[D];
+#pragma unroll
+        for (int col = 0; col < D; ++col) r64[col] = pts64[row * D + col];
+        const double delta = ci.delta;
+        const float hiA = __double2float_ru(__dadd_ru((double)t32_in[srow], 2.0 * delta));
+        // ---- phase A: exact k-th joint distance
+        double kd[S];
+#pragma unroll
+        for (int q = 0; q < S; ++q) kd[q] = (q < S - k) ? -INFINITY : INFINITY;
+        for (int base = 0; base < nsub; base += 32) {
+            const int st_l = base + lane;
+            bool need = false;
+            if (st_l < nsub) need = point_box<NG, NP>(ref, __ldg(fb + 2 * st_l), __ldg(fb + 2 * st_l + 1)) <= hiA;
+            uint32_t m = __ballot_sync(0xffffffffu, need);
+            while (m) {
+                const int st = base + __ffs(m) - 1;
+                m &= m - 1;
+                const int j = st * kSub + lane;
+                const float *q = cp + (int64_t)j * DP;
+                float d = 0.0f;
+#pragma unroll
+                for (int col = 0; col < D; ++col) {
+                    const float x = (col & 1) ? ref[col >> 1].y : ref[col >> 1].x;
+                    d = fmaxf(d, fabsf(q[col] + x));
+                }
+                if (j < ci.n && j != s && d <= hiA) {
+                    const double *q64 = pts64 + (ci.row0 + perm[ci.row0 + j]) * D;
+                    double d64 = 0.0;
+#pragma unroll
+                    for (int col = 0; col < D; ++col) d64 = fmax(d64, fabs(__dsub_rn(r64[col], q64[col])));
+                    if (d64 < kd[S - 1]) {
+#pragma unroll
+                        for (int q2 = S - 1; q2 >= 1; --q2) kd[q2] = fmax(kd[q2 - 1], fmin(kd[q2], d64));
+                        kd[0] = fmin(kd[0], d64);
+                    }
+                }
+            }
+        }
+        double eps = 0.0;
+        for (int q = 0; q < k; ++q) {
+            const double v = kd[S - k];
+            double mn = v;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+            const unsigned win = __ffs(__ballot_sync(0xffffffffu, v == mn)) - 1;
+            if ((unsigned)lane == win) {
+#pragma unroll
+                for (int q2 = 0; q2 < S - 1; ++q2)
+                    if (q2 >= S - k) kd[q2] = kd[q2 + 1];
+                kd[S - 1] = INFINITY;
+            }
+            eps = mn;
+        }
+        // ---- phase B: strict counts in the three TE marginals
+        const float lo = __double2float_rd(__dsub_rd(eps, delta));
+        const float hi = __double2float_ru(__dadd_ru(eps, delta));
+        int cnt[3] = {0, 0, 0};
+        for (int base = 0; base < nsub; base += 32) {
+            const int st_l = base + lane;
+            bool need = false;
+            if (st_l < nsub) need = point_box<NG, NP>(ref, __ldg(fb + 2 * st_l), __ldg(fb + 2 * st_l + 1)) <= hi;
+            uint32_t m = __ballot_sync(0xffffffffu, need);
+            while (m) {
+                const int st = base + __ffs(m) - 1;
+                m &= m - 1;
+                const int j = st * kSub + lane;
+                if (j >= ci.n || j == s) continue;
+                const float *q = cp + (int64_t)j * DP;
+                float a = 0.0f, b = 0.0f;
+#pragma unroll
+                for (int col = 1; col < D; ++col) {
+                    const float x = (col & 1) ? ref[col >> 1].y : ref[col >> 1].x;
+                    const float v = fabsf(q[col] + x);
+                    if (col <= DY) a = fmaxf(a, v);
+                    else b = fmaxf(b, v);
+                }
+                const float y = fabsf(q[0] + ref[0].x);
+                const float v32[3] = {a, fmaxf(a, y), fmaxf(a, b)};
+                bool amb = false;
+#pragma unroll
+                for (int o = 0; o < 3; ++o) {
+                    cnt[o] += v32[o] < lo;
+                    amb |= (v32[o] >= lo && v32[o] <= hi);
+                }
+                if (amb) {
+                    double A, m2, m3, jd;
+                    te_dist64(r64, pts64 + (ci.row0 + perm[ci.row0 + j]) * D, D, DY, A, m2, m3, jd);
+                    const double v64[3] = {A, m2, m3};
+#pragma unroll
+                    for (int o = 0; o < 3; ++o)
+                        cnt[o] += (v32[o] >= lo && v32[o] <= hi) && (v64[o] < eps);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) cnt[o] += __shfl_xor_sync(0xffffffffu, cnt[o], off);
+        }
+        if (lane == 0) {
+            out_eps[row] = eps;
+            for (int o = 0; o < lay.nout; ++o) out_counts[o * total_rows + row] = cnt[lay.slot[o]];
+        }
+        __syncwarp();
+    }
+}
 // ---------------------------------------------------------------------------
 // exact: one warp per point, fp64 scan, warp-shuffle top-k merge
 // ---------------------------------------------------------------------------
@@ -900,9 +1070,9 @@ __global__ void __launch_bounds__(kExactWarps * 32) exact_kernel(
 // ---------------------------------------------------------------------------
 // host side: kernel tables and dispatch
 // ---------------------------------------------------------------------------
-using KnnFn = void (*)(const float *, const float *, const ChunkInfo *, const TileRef *, int, int,
-                       float *, int32_t *, unsigned long long *);
-using CountFn = void (*)(const float *, const float *, const ChunkInfo *, const TileRef *,
+using KnnFn = void (*)(const float *, const float *, const ChunkInfo *, const int32_t *, int, int,
+                       int, float *, int32_t *, unsigned long long *);
+using CountFn = void (*)(const float *, const float *, const ChunkInfo *, const int32_t *, int,
                          const float *, int64_t, int, int32_t *, uint32_t *, int32_t *, uint32_t,
                          unsigned long long *);
 
@@ -923,6 +1093,25 @@ static KnnFn knn_for_slots(int slots) {
 static KnnFn knn_table(int dy, int dx, int slots) {
 #define ENTE_CASE(a, b) \
     if (dy == a && dx == b) return knn_for_slots<a, b>(slots);
+    ENTE_TE_LAYOUTS(ENTE_CASE)
+#undef ENTE_CASE
+    return nullptr;
+}
+
+using RescanFn = void (*)(const float *, const float *, const double *, const ChunkInfo *, int,
+                          const int32_t *, const float *, const int64_t *, const int32_t *, int,
+                          TeLayout, int64_t, double *, int32_t *);
+
+template <int DY, int DX>
+static RescanFn rescan_for_k(int k) {
+    if (k <= 4) return rescan_kernel<DY, DX, 4>;
+    if (k <= 8) return rescan_kernel<DY, DX, 8>;
+    return rescan_kernel<DY, DX, 16>;
+}
+
+static RescanFn rescan_table(int dy, int dx, int k) {
+#define ENTE_CASE(a, b) \
+    if (dy == a && dx == b) return rescan_for_k<a, b>(k);
     ENTE_TE_LAYOUTS(ENTE_CASE)
 #undef ENTE_CASE
     return nullptr;
@@ -1021,7 +1210,7 @@ static Plan make_plan(const ente_chunk *chunks, int n_chunks, int dim, const uin
 struct SearchWs {
     ChunkInfo *info;
     ColStats *stats;
-    TileRef *tiles;
+    int32_t *tile0;
     float *pts32;
     float *fbox;
     uint32_t *ka, *kb;
@@ -1034,15 +1223,18 @@ struct SearchWs {
     int32_t *ev_n;
     int64_t *ovf;
     int32_t *ovf_n;
+    int64_t *rs;
+    int32_t *rs_n;
 };
 
 static SearchWs layout_ws(Arena &a, const Plan &p, int n_chunks) {
     SearchWs w{};
     w.info = a.take<ChunkInfo>(n_chunks);
-    w.ovf_n = a.take<int32_t>(1);
+    w.ovf_n = a.take<int32_t>(2);
+    w.rs_n = w.ovf_n ? w.ovf_n + 1 : nullptr;
     if (p.fast) {
         w.stats = a.take<ColStats>(n_chunks);
-        w.tiles = a.take<TileRef>(p.n_tiles);
+        w.tile0 = a.take<int32_t>(n_chunks + 1);
         w.pts32 = a.take<float>((size_t)p.total_prows * p.dp);
         w.fbox = a.take<float>((size_t)(p.total_prows / kSub) * 2 * kGate);
         w.ka = a.take<uint32_t>(p.total_rows);
@@ -1056,6 +1248,7 @@ static SearchWs layout_ws(Arena &a, const Plan &p, int n_chunks) {
         w.ev = a.take<uint32_t>((size_t)p.total_rows * kCap);
         w.ev_n = a.take<int32_t>(p.total_rows);
         w.ovf = a.take<int64_t>(p.total_rows);
+        w.rs = a.take<int64_t>(p.total_rows);
     }
     return w;
 }
@@ -1206,7 +1399,8 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
     // host-side chunk table, tile list and k checks
     std::vector<ChunkInfo> hinfo(n_chunks);
     std::vector<int32_t> hstatus(n_chunks, ENTE_CHUNK_OK);
-    std::vector<TileRef> htiles;
+    std::vector<int32_t> htile0(n_chunks + 1, 0);
+    int32_t ntiles = 0;
     int64_t prow = 0;
     for (int c = 0; c < n_chunks; ++c) {
         ChunkInfo &ci = hinfo[c];
@@ -1218,18 +1412,19 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
         ci.ok32 = 0;
         prow += ci.npad;
         if (k > ci.n - 1) hstatus[c] = ENTE_CHUNK_K_TOO_LARGE;
-        if (p.fast && hstatus[c] == ENTE_CHUNK_OK)
-            for (int r0 = 0; r0 < ci.n; r0 += kWarpRefs) htiles.push_back({c, r0});
+        htile0[c] = ntiles;
+        if (p.fast && hstatus[c] == ENTE_CHUNK_OK) ntiles += (ci.n + kWarpRefs - 1) / kWarpRefs;
     }
+    htile0[n_chunks] = ntiles;
     ENTE_CUDA(cudaMemcpyAsync(w.info, hinfo.data(), sizeof(ChunkInfo) * n_chunks,
                               cudaMemcpyHostToDevice, st));
     ENTE_CUDA(cudaMemcpyAsync(status, hstatus.data(), sizeof(int32_t) * n_chunks,
                               cudaMemcpyHostToDevice, st));
-    ENTE_CUDA(cudaMemsetAsync(w.ovf_n, 0, sizeof(int32_t), st));
+    ENTE_CUDA(cudaMemsetAsync(w.ovf_n, 0, 2 * sizeof(int32_t), st));
     Masks masks{};
     masks.n = n_marg;
     for (int m = 0; m < n_marg; ++m) masks.m[m] = marg_masks[m];
-    if (p.fast && !htiles.empty()) {
+    if (p.fast && ntiles > 0) {
         const int prune = prune_enabled();
         unsigned long long *work = device_work();
         if (!work) {
@@ -1250,26 +1445,34 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
                     gather_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.stats,
                                                          w.perm, p.dp, p.fc, w.pts32, w.fbox));
         ENTE_CUDA(cudaGetLastError());
-        ENTE_CUDA(cudaMemcpyAsync(w.tiles, htiles.data(), sizeof(TileRef) * htiles.size(),
+        ENTE_CUDA(cudaMemcpyAsync(w.tile0, htile0.data(), sizeof(int32_t) * (n_chunks + 1),
                                   cudaMemcpyHostToDevice, st));
-        const unsigned nt = (unsigned)htiles.size();
+        const unsigned nt = (unsigned)ntiles;
         ENTE_LAUNCH("knn_pass", st,
                     knn_table(p.dy, p.dx, p.slots)<<<nt, 32, 0, st>>>(w.pts32, w.fbox, w.info,
-                                                                     w.tiles, k, prune, w.t32,
+                                                                     w.tile0, n_chunks, k, prune, w.t32,
                                                                      w.L, work));
         ENTE_CUDA(cudaGetLastError());
         uint32_t fmask = 8u;
         for (int o = 0; o < p.lay.nout; ++o) fmask |= 1u << p.lay.slot[o];
         ENTE_LAUNCH("count_pass", st,
-                    count_table(p.dy, p.dx)<<<nt, 32, 0, st>>>(w.pts32, w.fbox, w.info, w.tiles,
+                    count_table(p.dy, p.dx)<<<nt, 32, 0, st>>>(w.pts32, w.fbox, w.info, w.tile0, n_chunks,
                                                                w.t32, ws_rows, prune, w.cnt3, w.ev,
                                                                w.ev_n, fmask, work + 1));
         ENTE_CUDA(cudaGetLastError());
         ENTE_LAUNCH("resolve", st,
-                    resolve_kernel<<<nt, kWarpRefs, 0, st>>>(pts64, dim, w.info, w.tiles, k, p.lay,
+                    resolve_kernel<<<nt, kWarpRefs, 0, st>>>(pts64, dim, w.info, w.tile0, n_chunks, k, p.lay,
                                                        w.perm, w.L, w.cnt3, w.ev, w.ev_n, ws_rows,
                                                        total_rows, out_eps, out_counts, w.ovf,
-                                                       w.ovf_n));
+                                                       w.ovf_n, w.rs, w.rs_n));
+        ENTE_CUDA(cudaGetLastError());
+        {
+            const unsigned rgrid = (unsigned)(num_sms() * 8);
+            ENTE_LAUNCH("rescan", st,
+                        rescan_table(p.dy, p.dx, k)<<<rgrid, kRescanWarps * 32, 0, st>>>(
+                            w.pts32, w.fbox, pts64, w.info, n_chunks, w.perm, w.t32, w.rs, w.rs_n,
+                            k, p.lay, total_rows, out_eps, out_counts));
+        }
         ENTE_CUDA(cudaGetLastError());
         dispatch_exact(k, st, pts64, dim, w.info, n_chunks, status, w.ovf, w.ovf_n, 0, masks,
                        total_rows, out_eps, out_counts);

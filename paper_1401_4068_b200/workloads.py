@@ -188,3 +188,37 @@ CONFIGS = {
                          "u=5..17 step 2, window (801,890), S=500", (3, 1), tuple(range(5, 18, 2)),
                    (801, 890), 500, n_pairs=20),
 }
+
+
+# ---------------------------------------------------------------------------
+# C3: the kNN + range-search sweep over chunk shapes
+# ---------------------------------------------------------------------------
+def c3_chunk(n: int, dim: int, c: int, tied: bool = False) -> np.ndarray:
+    """Chunk c of the (n, dim) cell: default_rng(SeedSequence((0, n, dim, c))) normals.
+
+    The tie variant rounds to one decimal, as the reference's criterion-6
+    generator does (test_acceptance.py:219-220).
+    """
+    pts = np.random.default_rng(np.random.SeedSequence((0, n, dim, c))).standard_normal((n, dim))
+    return np.round(pts, 1) if tied else pts
+
+
+def c3_marginals(dim: int, layout: str):
+    """Marginal column lists of a C3 cell.
+
+    "te":    d_y = d_x = (dim - 1) // 2, the three KSG marginals
+             (embedding.py:50-60; dim = 17 is the paper's 1 + 8 + 8)
+    "bench": one marginal, the first (dim - 1) // 2 columns (bench.py:56;
+             m = 8 at dim = 17, the `ente bench` default geometry)
+    "knn":   no marginal (kNN distances only)
+    """
+    h = (dim - 1) // 2
+    if layout == "te":
+        if dim % 2 == 0 or dim < 3:
+            raise ValueError("the te layout needs an odd dim >= 3")
+        return [list(range(1, 1 + h)), list(range(0, 1 + h)), list(range(1, dim))]
+    if layout == "bench":
+        return [list(range(max(1, h)))]
+    if layout == "knn":
+        return []
+    raise ValueError(f"unknown C3 layout {layout!r}")
