@@ -45,13 +45,54 @@ namespace ente {
 constexpr int kSub = 32;                    // candidate rows per sub-tile (one TMA copy)
 constexpr int kWarpRefs = 32 * kRT;         // references per sweep CTA (one warp)
 constexpr int kGate = 4;                    // gate columns in the Morton key and the boxes
+constexpr int kKnnQ = 2;                    // kNN sub-tile boxes: 4 * kKnnQ columns from 0
 
 // per-chunk column statistics (fp64): mean, min, max of the raw values
+constexpr int kPcaCols = 8;  // principal axes over the first <= 8 columns
+
 struct ColStats {
     double mean[kMaxDim];
     double lo[kMaxDim];
     double hi[kMaxDim];
+    float axis[2][kPcaCols];  // the two leading principal axes (kNN order)
+    int32_t use_pca;          // variance off the leading plane < kPcaResidual of lambda_1
 };
+
+// The kNN pass sorts by the principal-axis Morton key only when the chunk is
+// essentially two-dimensional (embedded low-dimensional dynamics, e.g. the
+// Lorenz system: residual ~ 0.01); noise-driven AR data (residual >= 0.3)
+// keeps the y-past Morton order of the count pass.
+constexpr double kPcaResidual = 0.05;
+
+// Two leading eigenvectors of a symmetric P x P matrix by power iteration
+// with deflation (P <= 8; ordering quality only, not exactness).
+__device__ int principal_axes(double (&cov)[kPcaCols][kPcaCols], int P, float (&axis)[2][kPcaCols]) {
+    double trace = 0.0, top = 0.0, lead = 0.0;
+    for (int i = 0; i < P; ++i) trace += cov[i][i];
+    for (int a = 0; a < 2; ++a) {
+        double v[kPcaCols];
+        for (int i = 0; i < kPcaCols; ++i) v[i] = (i < P) ? 1.0 + 0.1 * i + 0.37 * a * (i & 1) : 0.0;
+        double lam = 0.0;
+        for (int it = 0; it < 64; ++it) {
+            double w[kPcaCols], nrm = 0.0;
+            for (int i = 0; i < P; ++i) {
+                w[i] = 0.0;
+                for (int j = 0; j < P; ++j) w[i] += cov[i][j] * v[j];
+                nrm += w[i] * w[i];
+            }
+            nrm = sqrt(nrm);
+            if (!(nrm > 0.0)) break;
+            for (int i = 0; i < P; ++i) v[i] = w[i] / nrm;
+            lam = nrm;
+        }
+        for (int i = 0; i < kPcaCols; ++i) axis[a][i] = (i < P) ? (float)v[i] : 0.0f;
+        for (int i = 0; i < P; ++i)
+            for (int j = 0; j < P; ++j) cov[i][j] -= lam * v[i] * v[j];
+        top += lam;
+        if (a == 0) lead = lam;
+    }
+    return lead > 0.0 && (trace - top) < kPcaResidual * lead;
+}
 
 __global__ void __launch_bounds__(256) prep_kernel(const double *__restrict__ pts64, int dim,
                                                    ChunkInfo *__restrict__ info,
@@ -101,9 +142,48 @@ __global__ void __launch_bounds__(256) prep_kernel(const double *__restrict__ pt
         }
         return;
     }
-    if (stats)
+    if (stats) {
         for (int e = threadIdx.x; e < 3 * kMaxDim; e += blockDim.x)
             (&stats[c].mean[0])[e] = (&local.mean[0])[e];
+        // covariance of the first P columns -> two principal axes (kNN sort key)
+        const int P = dim < kPcaCols ? dim : kPcaCols;
+        __shared__ float wsum[8][kPcaCols * (kPcaCols + 1) / 2];
+        float acc[kPcaCols * (kPcaCols + 1) / 2];  // fp32: the axes only steer the order
+#pragma unroll
+        for (int e = 0; e < kPcaCols * (kPcaCols + 1) / 2; ++e) acc[e] = 0.0f;
+        for (int r = threadIdx.x; r < ci.n; r += blockDim.x) {
+            float x[kPcaCols];
+#pragma unroll
+            for (int i = 0; i < kPcaCols; ++i)
+                x[i] = i < P ? (float)(p[(int64_t)r * dim + i] - cs->mean[i]) : 0.0f;
+            int e = 0;
+#pragma unroll
+            for (int i = 0; i < kPcaCols; ++i)
+#pragma unroll
+                for (int j = 0; j <= i; ++j) acc[e++] += x[i] * x[j];
+        }
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+        for (int e = 0; e < kPcaCols * (kPcaCols + 1) / 2; ++e) {
+            float v = acc[e];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            if (lane == 0) wsum[wid][e] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double cov[kPcaCols][kPcaCols];
+            int e = 0;
+            for (int i = 0; i < kPcaCols; ++i)
+                for (int j = 0; j <= i; ++j) {
+                    double v = 0.0;
+                    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += wsum[w][e];
+                    cov[i][j] = cov[j][i] = v;
+                    ++e;
+                }
+            stats[c].use_pca = principal_axes(cov, P, stats[c].axis);
+        }
+    }
     if (threadIdx.x == 0 && stats) {
         // spread s = max |fl64(x - m)| is attained at a column extreme
         double smax = 0.0;
@@ -165,6 +245,144 @@ __global__ void __launch_bounds__(kSortThreads) sort_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// kNN order: Morton order of the projections on the chunk's two leading
+// principal axes (15 bits each).  Embedded dynamics concentrate near a
+// low-dimensional manifold; a 2-D order along it keeps 32-row sub-tiles
+// compact in every column, which the kNN pass's all-column boxes exploit.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t spread15(uint32_t v) {  // bits 0..14 -> even bits
+    v &= 0x7FFFu;
+    v = (v | (v << 8)) & 0x00FF00FFu;
+    v = (v | (v << 4)) & 0x0F0F0F0Fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+
+__global__ void __launch_bounds__(kSortThreads) sort_pca_kernel(
+    const double *__restrict__ pts64, int dim, const ChunkInfo *__restrict__ info,
+    const ColStats *__restrict__ stats, uint32_t *__restrict__ ka, uint32_t *__restrict__ kb,
+    int32_t *__restrict__ va, int32_t *__restrict__ vb, const int32_t *__restrict__ cperm,
+    int32_t *__restrict__ perm) {
+    __shared__ SortSmem sm;
+    __shared__ float red[4][kSortWarps];
+    const ChunkInfo ci = info[blockIdx.x];
+    if (!ci.ok32) return;
+    const ColStats *cs = stats + blockIdx.x;
+    if (!cs->use_pca) {  // keep the count pass's y-past Morton order
+        for (int i = threadIdx.x; i < ci.n; i += kSortThreads) perm[ci.row0 + i] = cperm[ci.row0 + i];
+        return;
+    }
+    const int P = dim < kPcaCols ? dim : kPcaCols;
+    const double *p = pts64 + ci.row0 * dim;
+    uint32_t *k0 = ka + ci.row0, *k1 = kb + ci.row0;
+    int32_t *v0 = va + ci.row0, *v1 = vb + ci.row0;
+    float mn0 = INFINITY, mx0 = -INFINITY, mn1 = INFINITY, mx1 = -INFINITY;
+    auto proj = [&](int i, float &z0, float &z1) {
+        z0 = 0.0f;
+        z1 = 0.0f;
+        for (int c = 0; c < P; ++c) {
+            const float x = (float)(p[(int64_t)i * dim + c] - cs->mean[c]);
+            z0 += cs->axis[0][c] * x;
+            z1 += cs->axis[1][c] * x;
+        }
+    };
+    for (int i = threadIdx.x; i < ci.n; i += kSortThreads) {
+        float z0, z1;
+        proj(i, z0, z1);
+        mn0 = fminf(mn0, z0);
+        mx0 = fmaxf(mx0, z0);
+        mn1 = fminf(mn1, z1);
+        mx1 = fmaxf(mx1, z1);
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        mn0 = fminf(mn0, __shfl_xor_sync(0xffffffffu, mn0, off));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mn1 = fminf(mn1, __shfl_xor_sync(0xffffffffu, mn1, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        red[0][wid] = mn0;
+        red[1][wid] = mx0;
+        red[2][wid] = mn1;
+        red[3][wid] = mx1;
+    }
+    __syncthreads();
+    for (int w = 0; w < kSortWarps; ++w) {
+        mn0 = fminf(mn0, red[0][w]);
+        mx0 = fmaxf(mx0, red[1][w]);
+        mn1 = fminf(mn1, red[2][w]);
+        mx1 = fmaxf(mx1, red[3][w]);
+    }
+    const float q = 32767.0f;
+    const float s0 = mx0 > mn0 ? q / (mx0 - mn0) : 0.0f;
+    const float s1 = mx1 > mn1 ? q / (mx1 - mn1) : 0.0f;
+    for (int i = threadIdx.x; i < ci.n; i += kSortThreads) {
+        float z0, z1;
+        proj(i, z0, z1);
+        const uint32_t a = (uint32_t)fminf(fmaxf((z0 - mn0) * s0, 0.0f), q);
+        const uint32_t b = (uint32_t)fminf(fmaxf((z1 - mn1) * s1, 0.0f), q);
+        k0[i] = (spread15(a) << 1) | spread15(b);
+        v0[i] = i;
+    }
+    __syncthreads();
+    const int par = cta_radix_sort<uint32_t, int32_t>(k0, k1, v0, v1, ci.n, 30, sm);
+    const int32_t *res = par ? v1 : v0;
+    for (int i = threadIdx.x; i < ci.n; i += kSortThreads) perm[ci.row0 + i] = res[i];
+}
+
+// kNN copy: fp32 rows in the kNN order + boxes over columns 0 .. 4*kKnnQ-1
+// (unused slots hold 0) + kmap (kNN position -> count-order position).
+// Runs after gather_kernel, which fills inv (row -> count-order position).
+__global__ void __launch_bounds__(kTJ) gather_knn_kernel(
+    const double *__restrict__ pts64, int dim, const ChunkInfo *__restrict__ info, int n_chunks,
+    const ColStats *__restrict__ stats, const int32_t *__restrict__ permk,
+    const int32_t *__restrict__ inv, int dp, float *__restrict__ pts32, float *__restrict__ fbox,
+    int32_t *__restrict__ kmap) {
+    constexpr int NB = 4 * kKnnQ;
+    for (int cidx = blockIdx.y; cidx < n_chunks; cidx += gridDim.y) {
+        const ChunkInfo ci = info[cidx];
+        const int stage = blockIdx.x;
+        if (!ci.ok32 || stage * kTJ >= ci.npad) continue;
+        const ColStats *cs = stats + cidx;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int s = stage * kTJ + threadIdx.x;
+        const bool valid = s < ci.n;
+        const int32_t o = valid ? permk[ci.row0 + s] : 0;
+        const int64_t orig = ci.row0 + o;
+        if (valid) kmap[ci.row0 + s] = inv[orig];
+        float *q = pts32 + (ci.prow0 + s) * dp;
+        const int64_t sub = ci.prow0 / kSub + stage * (kTJ / kSub) + warp;
+        for (int col = 0; col < dp; ++col) {
+            float v = 0.0f;
+            if (col < dim)
+                v = valid ? __double2float_rn(__dsub_rn(pts64[orig * dim + col], cs->mean[col]))
+                          : INFINITY;
+            q[col] = v;
+            if (col < NB) {  // warp-uniform
+                float lo = 0.0f, hi = 0.0f;
+                if (col < dim) {
+                    lo = valid ? v : INFINITY;
+                    hi = valid ? v : -INFINITY;
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+                        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+                    }
+                }
+                if (lane == 0) {
+                    fbox[sub * 2 * NB + col] = lo;
+                    fbox[sub * 2 * NB + NB + col] = hi;
+                }
+            }
+        }
+        if (lane == 0)
+            for (int col = dp; col < NB; ++col) fbox[sub * 2 * NB + col] = fbox[sub * 2 * NB + NB + col] = 0.0f;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // gather: sorted fp32 rows (centred, D padded to DP) + per-32-row boxes over
 // the gate columns (fbox layout per sub-tile: lo[kGate] | hi[kGate]; unused
 // gate slots hold 0 so they add nothing to a box distance)
@@ -174,7 +392,8 @@ __global__ void __launch_bounds__(kTJ) gather_kernel(const double *__restrict__ 
                                                      const ColStats *__restrict__ stats,
                                                      const int32_t *__restrict__ perm, int dp,
                                                      FilterCols fc, float *__restrict__ pts32,
-                                                     float *__restrict__ fbox) {
+                                                     float *__restrict__ fbox,
+                                                     int32_t *__restrict__ inv) {
     for (int cidx = blockIdx.y; cidx < n_chunks; cidx += gridDim.y) {
         const ChunkInfo ci = info[cidx];
         const int stage = blockIdx.x;
@@ -184,6 +403,7 @@ __global__ void __launch_bounds__(kTJ) gather_kernel(const double *__restrict__ 
         const int s = stage * kTJ + threadIdx.x;
         const bool valid = s < ci.n;
         const int64_t orig = valid ? ci.row0 + perm[ci.row0 + s] : 0;
+        if (valid && inv) inv[orig] = s;
         float *q = pts32 + (ci.prow0 + s) * dp;
         const int64_t sub = ci.prow0 / kSub + stage * (kTJ / kSub) + warp;
         for (int col = 0; col < dp; ++col) {
@@ -338,6 +558,31 @@ __device__ __forceinline__ float warp_max_nonneg(float v) {
 // are streamed into a ring of NSLOT shared-memory slots by the TMA engine
 // (cp.async.bulk + mbarrier).  Warps never wait for each other.
 // ---------------------------------------------------------------------------
+// A sub-tile box: Q float4 quads of column minima, then Q of maxima
+// (fbox layout per sub-tile: lo[4Q] | hi[4Q], float4 index st * 2Q).
+template <int Q>
+struct Box {
+    float4 lo[Q], hi[Q];
+};
+
+template <int Q>
+__device__ __forceinline__ Box<Q> load_box(const float4 *__restrict__ fb, int st) {
+    Box<Q> b;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        b.lo[q] = __ldg(fb + 2 * Q * st + q);
+        b.hi[q] = __ldg(fb + 2 * Q * st + Q + q);
+    }
+    return b;
+}
+
+__device__ __forceinline__ float gap4(float4 lo, float4 hi, float4 blo, float4 bhi) {
+    const float a = fmaxf(fmaxf(lo.x - bhi.x, blo.x - hi.x), fmaxf(lo.y - bhi.y, blo.y - hi.y));
+    const float b = fmaxf(fmaxf(lo.z - bhi.z, blo.z - hi.z), fmaxf(lo.w - bhi.w, blo.w - hi.w));
+    return fmaxf(a, b);
+}
+
+template <int Q>
 struct Walker {
     int h0, nh, nsub, npos;
     int base;       // first position of the evaluated window (-32 before the first)
@@ -345,8 +590,8 @@ struct Walker {
     int wst;        // per lane: sub-tile at position base + lane (-1: none)
     float wd;       // per lane: its box distance
     int nst;        // per lane: sub-tile at position base + 32 + lane (prefetched)
-    float4 nlo, nhi;
-    float4 blo, bhi;  // the warp's own box (gate columns), identical in all lanes
+    Box<Q> nb;      // its box
+    Box<Q> own;     // the warp's own box, identical in all lanes
 
     __device__ int sub_at(int pos) const {
         if (pos < nh) return h0 + pos;
@@ -357,10 +602,7 @@ struct Walker {
 
     __device__ void prefetch(const float4 *__restrict__ fb, int pos) {
         nst = pos < npos ? sub_at(pos) : -1;
-        if (nst >= 0) {
-            nlo = __ldg(fb + 2 * nst);
-            nhi = __ldg(fb + 2 * nst + 1);
-        }
+        if (nst >= 0) nb = load_box<Q>(fb, nst);
     }
 
     __device__ void init(const float4 *__restrict__ fb, int wrow, int n, int npad) {
@@ -370,27 +612,32 @@ struct Walker {
         npos = nh + 2 * max(h0, nsub - h0 - nh);
         base = -32;
         mask = 0;
-        blo = __ldg(fb + 2 * h0);
-        bhi = __ldg(fb + 2 * h0 + 1);
+        own = load_box<Q>(fb, h0);
         for (int s = 1; s < nh; ++s) {
-            const float4 l = __ldg(fb + 2 * (h0 + s)), h = __ldg(fb + 2 * (h0 + s) + 1);
-            blo = make_float4(fminf(blo.x, l.x), fminf(blo.y, l.y), fminf(blo.z, l.z), fminf(blo.w, l.w));
-            bhi = make_float4(fmaxf(bhi.x, h.x), fmaxf(bhi.y, h.y), fmaxf(bhi.z, h.z), fmaxf(bhi.w, h.w));
+            const Box<Q> b = load_box<Q>(fb, h0 + s);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                own.lo[q] = make_float4(fminf(own.lo[q].x, b.lo[q].x), fminf(own.lo[q].y, b.lo[q].y),
+                                        fminf(own.lo[q].z, b.lo[q].z), fminf(own.lo[q].w, b.lo[q].w));
+                own.hi[q] = make_float4(fmaxf(own.hi[q].x, b.hi[q].x), fmaxf(own.hi[q].y, b.hi[q].y),
+                                        fmaxf(own.hi[q].z, b.hi[q].z), fmaxf(own.hi[q].w, b.hi[q].w));
+            }
         }
         prefetch(fb, (threadIdx.x & 31));
     }
 
     // fp32 box distance (a lower bound of every d32 between the two boxes:
     // fl is monotone, fl(x_j - x_i) >= fl(lo_j - hi_i))
-    __device__ float dist(float4 lo, float4 hi) const {
-        const float a = fmaxf(fmaxf(lo.x - bhi.x, blo.x - hi.x), fmaxf(lo.y - bhi.y, blo.y - hi.y));
-        const float b = fmaxf(fmaxf(lo.z - bhi.z, blo.z - hi.z), fmaxf(lo.w - bhi.w, blo.w - hi.w));
-        return fmaxf(fmaxf(a, b), 0.0f);
+    __device__ float dist(const Box<Q> &b) const {
+        float d = 0.0f;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) d = fmaxf(d, gap4(b.lo[q], b.hi[q], own.lo[q], own.hi[q]));
+        return d;
     }
 
     // Next sub-tile whose box distance to the warp's box is below `bound`
     // (strict) or not above it, AND that some reference of the warp needs by
-    // its own point-to-box distance (refs_need(lo, hi), evaluated per lane);
+    // its own point-to-box distance (refs_need(box), evaluated per lane);
     // returns -1 when the walk is over.
     template <class RefTest>
     __device__ int next(const float4 *__restrict__ fb, float bound, bool strict,
@@ -401,7 +648,7 @@ struct Walker {
                 if (base + 32 >= npos) return -1;
                 base += 32;
                 wst = nst;
-                wd = wst >= 0 ? dist(nlo, nhi) : INFINITY;
+                wd = wst >= 0 ? dist(nb) : INFINITY;
                 mask = __ballot_sync(0xffffffffu, strict ? (wd < bound) : (wd <= bound));
                 prefetch(fb, base + 32 + lane);
             }
@@ -410,25 +657,26 @@ struct Walker {
             const float d = __shfl_sync(0xffffffffu, wd, b);
             if (!(strict ? (d < bound) : (d <= bound))) continue;  // the bound may have shrunk
             const int st = __shfl_sync(0xffffffffu, wst, b);
-            const float4 lo = __ldg(fb + 2 * st), hi = __ldg(fb + 2 * st + 1);
-            if (__any_sync(0xffffffffu, refs_need(lo, hi))) return st;
+            if (__any_sync(0xffffffffu, refs_need(load_box<Q>(fb, st)))) return st;
         }
     }
 };
 
 // fp32 distance from a reference (negated packed coordinates) to a sub-tile
-// box over the gate columns 1 .. NG (NG <= kGate): a lower bound of the
-// reference's fp32 distance to every row of the sub-tile (fl monotone).
-template <int NG, int NP>
-__device__ __forceinline__ float point_box(const float2 (&nr)[NP], float4 lo, float4 hi) {
-    const float l[4] = {lo.x, lo.y, lo.z, lo.w};
-    const float h[4] = {hi.x, hi.y, hi.z, hi.w};
+// box over the columns F0 .. F0 + NC - 1 (box slot g = column - F0): a lower
+// bound of the reference's fp32 distance to every row of the sub-tile over
+// any column set containing them (fl monotone).
+template <int F0, int NC, int NP, int Q>
+__device__ __forceinline__ float point_box(const float2 (&nr)[NP], const Box<Q> &b) {
     float d = 0.0f;
 #pragma unroll
-    for (int g = 0; g < NG; ++g) {
-        const int c = 1 + g;  // column
+    for (int g = 0; g < NC; ++g) {
+        const int c = F0 + g;  // column
         const float x = (c & 1) ? nr[c >> 1].y : nr[c >> 1].x;  // -x_c
-        const float2 e = __fadd2_rn(make_float2(l[g], h[g]), make_float2(x, x));  // lo-x, hi-x
+        const float4 l4 = b.lo[g >> 2], h4 = b.hi[g >> 2];
+        const float l = (g & 3) == 0 ? l4.x : (g & 3) == 1 ? l4.y : (g & 3) == 2 ? l4.z : l4.w;
+        const float h = (g & 3) == 0 ? h4.x : (g & 3) == 1 ? h4.y : (g & 3) == 2 ? h4.z : h4.w;
+        const float2 e = __fadd2_rn(make_float2(l, h), make_float2(x, x));  // lo-x, hi-x
         d = fmaxf(fmaxf(d, e.x), -e.y);
     }
     return d;
@@ -456,16 +704,18 @@ template <int DY, int DX, int S>
 __global__ void __launch_bounds__(32) knn_pass_kernel(
     const float *__restrict__ pts32, const float *__restrict__ fbox,
     const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks, int k, int prune,
-    float *__restrict__ t32_out, int32_t *__restrict__ L_out, unsigned long long *__restrict__ work) {
+    const int32_t *__restrict__ kmap, float *__restrict__ t32_out, int32_t *__restrict__ L_out,
+    unsigned long long *__restrict__ work) {
     using L = Lay<DY, DX>;
     constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG, NSLOT = L::NSLOT;
+    constexpr int NBC = D < 4 * kKnnQ ? D : 4 * kKnnQ;  // box columns 0 .. NBC-1
     __shared__ __align__(128) Ring<DP, NSLOT> ring;
     const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
     const int lane = threadIdx.x;
     const float *cp = pts32 + ci.prow0 * DP;
-    const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2;
+    const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2 * kKnnQ;
     const int wrow = tr.r0;
     float2 ref[kRT][NP];
     float kd[kRT][S];
@@ -480,14 +730,13 @@ __global__ void __launch_bounds__(32) knn_pass_kernel(
     if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
     fence_barrier_init();
     __syncwarp();
-    Walker wk;
+    Walker<kKnnQ> wk;
     wk.init(fb, wrow, ci.n, ci.npad);
-    constexpr int NG = DY < kGate ? DY : kGate;
     float bound = INFINITY;  // warp max of the current k-th distances
-    auto refs_need = [&](float4 lo, float4 hi) {
+    auto refs_need = [&](const Box<kKnnQ> &b) {
         bool need = !prune;
 #pragma unroll
-        for (int r = 0; r < kRT; ++r) need |= point_box<NG, NP>(ref[r], lo, hi) < kd[r][S - 1];
+        for (int r = 0; r < kRT; ++r) need |= point_box<0, NBC, NP, kKnnQ>(ref[r], b) < kd[r][S - 1];
         return need;
     };
     int slot_st = -1;        // lane s: sub-tile in ring slot s
@@ -566,8 +815,9 @@ __global__ void __launch_bounds__(32) knn_pass_kernel(
 #pragma unroll
         for (int s = 0; s < S; ++s) Lc += (kd[r][s] > -INFINITY) && (kd[r][s] < lo);
         if (lo > 0.0f) Lc -= 1;  // the self pair (distance 0) was counted
-        t32_out[ci.row0 + idx] = t32;
-        L_out[ci.row0 + idx] = Lc;
+        const int64_t orow = ci.row0 + (kmap ? kmap[ci.row0 + idx] : idx);  // count-order row
+        t32_out[orow] = t32;
+        L_out[orow] = Lc;
     }
 }
 
@@ -578,7 +828,7 @@ __global__ void __launch_bounds__(32) knn_pass_kernel(
 //   everywhere, no event) after the gate columns alone
 // ---------------------------------------------------------------------------
 template <int DY, int DX>
-__global__ void __launch_bounds__(32) count_pass_kernel(
+__global__ void __launch_bounds__(32, 21) count_pass_kernel(
     const float *__restrict__ pts32, const float *__restrict__ fbox,
     const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks,
     const float *__restrict__ t32_in, int64_t ws_rows, int prune, int32_t *__restrict__ cnt_out,
@@ -618,16 +868,16 @@ __global__ void __launch_bounds__(32) count_pass_kernel(
     }
     const float bound = warp_max_nonneg(hmax);
     constexpr int NG = DY < kGate ? DY : kGate;
-    auto refs_need = [&](float4 lo, float4 hi) {
+    auto refs_need = [&](const Box<1> &b) {
         bool need = !prune;
 #pragma unroll
-        for (int r = 0; r < kRT; ++r) need |= point_box<NG, NP>(ref[r], lo, hi) <= band[r].hi;
+        for (int r = 0; r < kRT; ++r) need |= point_box<1, NG, NP, 1>(ref[r], b) <= band[r].hi;
         return need;
     };
     if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
     fence_barrier_init();
     __syncwarp();
-    Walker wk;
+    Walker<1> wk;
     wk.init(fb, wrow, ci.n, ci.npad);
     int slot_st = -1;
     int issued = 0;
@@ -881,7 +1131,7 @@ __global__ void __launch_bounds__(kRescanWarps * 32) rescan_kernel(
         for (int base = 0; base < nsub; base += 32) {
             const int st_l = base + lane;
             bool need = false;
-            if (st_l < nsub) need = point_box<NG, NP>(ref, __ldg(fb + 2 * st_l), __ldg(fb + 2 * st_l + 1)) <= hiA;
+            if (st_l < nsub) need = point_box<1, NG, NP, 1>(ref, load_box<1>(fb, st_l)) <= hiA;
             uint32_t m = __ballot_sync(0xffffffffu, need);
             while (m) {
                 const int st = base + __ffs(m) - 1;
@@ -929,7 +1179,7 @@ __global__ void __launch_bounds__(kRescanWarps * 32) rescan_kernel(
         for (int base = 0; base < nsub; base += 32) {
             const int st_l = base + lane;
             bool need = false;
-            if (st_l < nsub) need = point_box<NG, NP>(ref, __ldg(fb + 2 * st_l), __ldg(fb + 2 * st_l + 1)) <= hi;
+            if (st_l < nsub) need = point_box<1, NG, NP, 1>(ref, load_box<1>(fb, st_l)) <= hi;
             uint32_t m = __ballot_sync(0xffffffffu, need);
             while (m) {
                 const int st = base + __ffs(m) - 1;
@@ -1071,7 +1321,7 @@ __global__ void __launch_bounds__(kExactWarps * 32) exact_kernel(
 // host side: kernel tables and dispatch
 // ---------------------------------------------------------------------------
 using KnnFn = void (*)(const float *, const float *, const ChunkInfo *, const int32_t *, int, int,
-                       int, float *, int32_t *, unsigned long long *);
+                       int, const int32_t *, float *, int32_t *, unsigned long long *);
 using CountFn = void (*)(const float *, const float *, const ChunkInfo *, const int32_t *, int,
                          const float *, int64_t, int, int32_t *, uint32_t *, int32_t *, uint32_t,
                          unsigned long long *);
@@ -1225,6 +1475,9 @@ struct SearchWs {
     int32_t *ovf_n;
     int64_t *rs;
     int32_t *rs_n;
+    // kNN order (principal-axis Morton)
+    int32_t *permk, *kmap, *inv;
+    float *pts32k, *fboxk;
 };
 
 static SearchWs layout_ws(Arena &a, const Plan &p, int n_chunks) {
@@ -1249,6 +1502,11 @@ static SearchWs layout_ws(Arena &a, const Plan &p, int n_chunks) {
         w.ev_n = a.take<int32_t>(p.total_rows);
         w.ovf = a.take<int64_t>(p.total_rows);
         w.rs = a.take<int64_t>(p.total_rows);
+        w.permk = a.take<int32_t>(p.total_rows);
+        w.kmap = a.take<int32_t>(p.total_rows);
+        w.inv = a.take<int32_t>(p.total_rows);
+        w.pts32k = a.take<float>((size_t)p.total_prows * p.dp);
+        w.fboxk = a.take<float>((size_t)(p.total_prows / kSub) * 2 * 4 * kKnnQ);
     }
     return w;
 }
@@ -1440,17 +1698,28 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
                     sort_kernel<<<n_chunks, kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats, sfc,
                                                                    w.ka, w.kb, w.va, w.vb, w.perm));
         ENTE_CUDA(cudaGetLastError());
+        ENTE_LAUNCH("sort_pca", st,
+                    sort_pca_kernel<<<n_chunks, kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats,
+                                                                       w.ka, w.kb, w.va, w.vb,
+                                                                       w.perm, w.permk));
+        ENTE_CUDA(cudaGetLastError());
         dim3 ggrid((unsigned)(p.max_npad / kTJ), (unsigned)std::min(n_chunks, 65535));
         ENTE_LAUNCH("gather", st,
                     gather_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.stats,
-                                                         w.perm, p.dp, p.fc, w.pts32, w.fbox));
+                                                         w.perm, p.dp, p.fc, w.pts32, w.fbox,
+                                                         w.inv));
+        ENTE_CUDA(cudaGetLastError());
+        ENTE_LAUNCH("gather_knn", st,
+                    gather_knn_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.stats,
+                                                             w.permk, w.inv, p.dp, w.pts32k,
+                                                             w.fboxk, w.kmap));
         ENTE_CUDA(cudaGetLastError());
         ENTE_CUDA(cudaMemcpyAsync(w.tile0, htile0.data(), sizeof(int32_t) * (n_chunks + 1),
                                   cudaMemcpyHostToDevice, st));
         const unsigned nt = (unsigned)ntiles;
         ENTE_LAUNCH("knn_pass", st,
-                    knn_table(p.dy, p.dx, p.slots)<<<nt, 32, 0, st>>>(w.pts32, w.fbox, w.info,
-                                                                     w.tile0, n_chunks, k, prune, w.t32,
+                    knn_table(p.dy, p.dx, p.slots)<<<nt, 32, 0, st>>>(w.pts32k, w.fboxk, w.info,
+                                                                     w.tile0, n_chunks, k, prune, w.kmap, w.t32,
                                                                      w.L, work));
         ENTE_CUDA(cudaGetLastError());
         uint32_t fmask = 8u;

@@ -15,6 +15,7 @@ bit-identical to the reference's fp64 sweep.
 from __future__ import annotations
 
 import os
+import threading
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -108,32 +109,53 @@ def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int, reuse: bool = F
     return eps, counts[:len(masks)], status[:len(ns)]
 
 
+class _Pinned(threading.local):
+    buf = None
+
+
+_pinned = _Pinned()
+
+
+def _pinned_buffer(nbytes: int) -> torch.Tensor:
+    """Grow-only pinned host staging buffer (page-locking per call costs more than the copy)."""
+    buf = _pinned.buf
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8).pin_memory()
+        _pinned.buf = buf
+    return buf
+
+
 def _upload(points_list):
-    host = np.ascontiguousarray(np.concatenate(points_list, axis=0), dtype=np.float64)
-    t = torch.from_numpy(host)
-    if torch.cuda.is_available():
-        t = t.pin_memory()
-    return t.to(nat.device(), non_blocking=True)
+    """Concatenate the chunks straight into pinned memory and copy them to the device."""
+    rows = sum(p.shape[0] for p in points_list)
+    dim = points_list[0].shape[1]
+    stage = _pinned_buffer(rows * dim * 8)[:rows * dim * 8].view(torch.float64).view(rows, dim)
+    np.concatenate(points_list, axis=0, out=stage.numpy())
+    dev = nat.scratch("engine.points", (rows, dim), torch.float64)
+    dev.copy_(stage, non_blocking=True)
+    return dev
 
 
 def _run_group(points_list, dim, masks, k):
-    ns = [p.shape[0] for p in points_list]
+    ns = np.fromiter((p.shape[0] for p in points_list), dtype=np.int64, count=len(points_list))
     rows0 = np.concatenate([[0], np.cumsum(ns)[:-1]]).astype(np.int64)
     dev = _upload(points_list)
-    eps, counts, status = search_device(dev, rows0, ns, masks, k)
+    eps, counts, status = search_device(dev, rows0, ns, masks, k, reuse=True)
     eps_h = eps.cpu().numpy()
     cnt_h = counts.cpu().numpy().astype(np.int64)
     st_h = status.cpu().numpy()
     out = []
-    for i, (r0, n) in enumerate(zip(rows0, ns)):
+    nm = len(masks)
+    for i in range(len(points_list)):
+        r0, n = int(rows0[i]), int(ns[i])
         if st_h[i] == nat.CHUNK_NONFINITE:
             out.append(ShapeMismatch("chunk contains non-finite values"))
         elif st_h[i] == nat.CHUNK_K_TOO_LARGE:
             out.append(KTooLarge(f"k={k} not in [1, n-1] for n={n}"))
         else:
-            sl = slice(r0, r0 + n)
-            out.append(NeighborCounts(eps_h[sl].copy(), tuple(cnt_h[m, sl].copy()
-                                                              for m in range(len(masks)))))
+            # views into this call's fresh result arrays (nothing else holds them)
+            out.append(NeighborCounts(eps_h[r0:r0 + n],
+                                      tuple(cnt_h[m, r0:r0 + n] for m in range(nm))))
     return out
 
 
@@ -146,17 +168,25 @@ def batch_search(items: Sequence, k: int):
     """
     results = [None] * len(items)
     groups = {}
+    mask_cache = {}  # (id(marginals), dim) -> (marginals, masks): items usually share one list
     for slot, (chunk, marginals) in enumerate(items):
-        pts = np.ascontiguousarray(np.asarray(chunk.points, dtype=np.float64))
+        pts = chunk.points
+        if not (isinstance(pts, np.ndarray) and pts.dtype == np.float64 and pts.flags.c_contiguous):
+            pts = np.ascontiguousarray(np.asarray(pts, dtype=np.float64))
         n, dim = pts.shape
         if k < 1 or k > n - 1:
             results[slot] = KTooLarge(f"k={k} not in [1, n-1] for n={n}")
             continue
-        try:
-            masks = tuple(column_mask(cols, dim) for cols in marginals)
-        except ShapeMismatch as exc:
-            results[slot] = exc
-            continue
+        hit = mask_cache.get((id(marginals), dim))
+        if hit is not None and hit[0] is marginals:
+            masks = hit[1]
+        else:
+            try:
+                masks = tuple(column_mask(cols, dim) for cols in marginals)
+            except ShapeMismatch as exc:
+                results[slot] = exc
+                continue
+            mask_cache[(id(marginals), dim)] = (marginals, masks)
         if dim > MAX_DIM or k > MAX_K or len(masks) > MAX_MARG:
             results[slot] = NotImplementedError(
                 f"dim={dim} (<= {MAX_DIM}), k={k} (<= {MAX_K}), marginals={len(masks)} "

@@ -10,7 +10,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 wl = workloads.CONFIGS[name]
 x, y = wl.ensembles()
 spec = EmbeddingSpec(*wl.spec)
-s = wl.n_surrogates
+s = int(sys.argv[2]) if len(sys.argv) > 2 else wl.n_surrogates
 cfg = AnalysisConfig(u_candidates=wl.u_candidates, window=wl.window, k=wl.k, n_surrogates=s, seed=0)
 pipe = PairPipeline(EnsembleSeries("X", x), EnsembleSeries("Y", y), spec, spec, cfg)
 pipe.set_perms([cached_permutation(0, i, x.shape[0], True) for i in range(s)])
