@@ -63,7 +63,7 @@ extern "C" int ente_microbench_pce(int iters, int blocks, double *pce_per_s, voi
     ENTE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     if (blocks <= 0) blocks = sms * 8;
     float *out = nullptr;
-    ENTE_CUDA(cudaMallocAsync(&out, sizeof(float) * blocks * 128, st));
+    ENTE_CUDA(cudaMalloc(&out, sizeof(float) * blocks * 128));
     cudaEvent_t a, b;
     ENTE_CUDA(cudaEventCreate(&a));
     ENTE_CUDA(cudaEventCreate(&b));
@@ -76,7 +76,7 @@ extern "C" int ente_microbench_pce(int iters, int blocks, double *pce_per_s, voi
     ENTE_CUDA(cudaEventElapsedTime(&ms, a, b));
     cudaEventDestroy(a);
     cudaEventDestroy(b);
-    ENTE_CUDA(cudaFreeAsync(out, st));
+    ENTE_CUDA(cudaFree(out));
     const double pce = (double)blocks * 128 * 4 * kMbDim * (double)kMbCands * iters;
     *pce_per_s = pce / (ms * 1e-3);
     return ENTE_OK;

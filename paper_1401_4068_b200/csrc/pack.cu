@@ -10,6 +10,7 @@
 // shuffling the target's repetitions permutes only the y columns.
 #include <cuda_runtime.h>
 
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -50,6 +51,30 @@ __global__ void __launch_bounds__(256) pack_te_kernel(
 
 using namespace ente;
 
+// Per-device grow-only item table.  Stream-ordered use on one stream per
+// device (the library's contract): a later copy into the table is ordered
+// after the earlier kernel that read it.
+static PackItem *item_table(int n) {
+    static std::mutex mu;
+    static PackItem *tab[64] = {nullptr};
+    static int cap[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (cap[dev] < n) {
+        if (tab[dev]) cudaFree(tab[dev]);  // synchronises: rare (growth only)
+        tab[dev] = nullptr;
+        cap[dev] = 0;
+        const int want = n < 4096 ? 4096 : n + n / 2;
+        void *p = nullptr;
+        if (cudaMalloc(&p, sizeof(PackItem) * (size_t)want) != cudaSuccess) return nullptr;
+        tab[dev] = static_cast<PackItem *>(p);
+        cap[dev] = want;
+    }
+    return tab[dev];
+}
+
 extern "C" int ente_pack_te_items(const double *x, const double *y, int reps, int n_samples,
                                   int dx, int tau_x, int dy, int tau_y, int w,
                                   const int32_t *items, int n_items, const int32_t *perms,
@@ -77,9 +102,15 @@ extern "C" int ente_pack_te_items(const double *x, const double *y, int reps, in
         h[i] = PackItem{u, perm, t_lo, 0};
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // items travel as kernel-visible memory via a small stream-ordered copy
-    PackItem *ditems = nullptr;
-    ENTE_CUDA(cudaMallocAsync(&ditems, sizeof(PackItem) * n_items, st));
+    // items travel through a per-device, grow-only device table with a
+    // stream-ordered copy (no per-call allocation: stream-ordered
+    // allocations are trimmed at every synchronisation, which cost
+    // 10-600 ms per call)
+    PackItem *ditems = item_table(n_items);
+    if (!ditems) {
+        set_error("ente_pack_te: cannot allocate the item table (%d items)", n_items);
+        return ENTE_ERR_CUDA;
+    }
     ENTE_CUDA(cudaMemcpyAsync(ditems, h.data(), sizeof(PackItem) * n_items, cudaMemcpyHostToDevice, st));
     const int64_t rows = (int64_t)reps * w;
     dim3 grid((unsigned)((rows + 255) / 256), (unsigned)(n_items < 65535 ? n_items : 65535));
@@ -87,7 +118,6 @@ extern "C" int ente_pack_te_items(const double *x, const double *y, int reps, in
                 pack_te_kernel<<<grid, 256, 0, st>>>(x, y, reps, n_samples, dx, tau_x, dy, tau_y, w,
                                                      ditems, n_items, perms, out));
     ENTE_CUDA(cudaGetLastError());
-    ENTE_CUDA(cudaFreeAsync(ditems, st));
     // (a pageable-source cudaMemcpyAsync has staged h before returning)
     return ENTE_OK;
 }

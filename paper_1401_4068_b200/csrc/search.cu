@@ -45,6 +45,13 @@ namespace ente {
 constexpr int kSub = 32;                    // candidate rows per sub-tile (one TMA copy)
 constexpr int kWarpRefs = 32 * kRT;         // references per sweep CTA (one warp)
 constexpr int kGate = 4;                    // gate columns in the Morton key and the boxes
+// minimum resident sweep CTAs (one warp each) per SM: caps the registers
+#ifndef ENTE_CNT_MINB
+#define ENTE_CNT_MINB 21
+#endif
+#ifndef ENTE_KNN_MINB
+#define ENTE_KNN_MINB 21
+#endif
 constexpr int kKnnQ = 2;                    // kNN sub-tile boxes: 4 * kKnnQ columns from 0
 
 // per-chunk column statistics (fp64): mean, min, max of the raw values
@@ -701,7 +708,7 @@ __device__ __forceinline__ void ring_issue(Ring<DP, NSLOT> &ring, int slot, cons
 // lane l owns sorted rows wrow + r*32 + l, r < kRT
 // ---------------------------------------------------------------------------
 template <int DY, int DX, int S>
-__global__ void __launch_bounds__(32) knn_pass_kernel(
+__global__ void __launch_bounds__(32, ENTE_KNN_MINB) knn_pass_kernel(
     const float *__restrict__ pts32, const float *__restrict__ fbox,
     const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks, int k, int prune,
     const int32_t *__restrict__ kmap, float *__restrict__ t32_out, int32_t *__restrict__ L_out,
@@ -828,7 +835,7 @@ __global__ void __launch_bounds__(32) knn_pass_kernel(
 //   everywhere, no event) after the gate columns alone
 // ---------------------------------------------------------------------------
 template <int DY, int DX>
-__global__ void __launch_bounds__(32, 21) count_pass_kernel(
+__global__ void __launch_bounds__(32, ENTE_CNT_MINB) count_pass_kernel(
     const float *__restrict__ pts32, const float *__restrict__ fbox,
     const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks,
     const float *__restrict__ t32_in, int64_t ws_rows, int prune, int32_t *__restrict__ cnt_out,
