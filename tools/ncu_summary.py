@@ -11,6 +11,19 @@ STALL = "smsp__average_warps_issue_stalled_"
 out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 hdr, units = rows[0], rows[1]
+if "--traffic" in sys.argv:  # {kernel: dram read+write bytes per launch} for bench.py
+    import json
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    res = {}
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        name = d["Kernel Name"].split("<")[0].replace("void ", "").split("(")[0].strip()
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(d[k].replace(",", "")) * scale.get(units[hdr.index(k)], 1)
+        res.setdefault(name, tot)
+    print(json.dumps(res))
+    sys.exit(0)
 for r in rows[2:]:
     d = dict(zip(hdr, r))
     print("==", d["Kernel Name"][:70])
