@@ -192,7 +192,7 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # roofline of the dominant sweep (FP32 CUDA-core / issue bound)
 # ---------------------------------------------------------------------------
-def roofline_of(prof, steps, pce_step, knn_sub, cnt_sub, dim, local):
+def roofline_of(prof, steps, pce_step, knn_pairs, cnt_pairs, dim, local):
     """roofline JSON object of the dominant sweep kernel.
 
     pce_step: algorithmic pair-coordinate evaluations per step for each
@@ -221,10 +221,9 @@ def roofline_of(prof, steps, pce_step, knn_sub, cnt_sub, dim, local):
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(dom)
     total_ms = sum(v["ms"] for v in prof.values())
-    # pruned work actually evaluated: sub-tiles of 32 candidates x 128 references
-    sub_pce = 32 * 128 * dim
-    evaluated = {k: n * sub_pce / max(1, prof.get(k, {}).get("launches", 1))
-                 for k, n in (("knn_pass", knn_sub), ("count_pass", cnt_sub))}
+    # pruned work actually evaluated: pairs of whole sub-tiles x reference groups
+    evaluated = {k: n * dim / max(1, prof.get(k, {}).get("launches", 1))
+                 for k, n in (("knn_pass", knn_pairs), ("count_pass", cnt_pairs))}
     ev_rate = 2.0 * evaluated[dom] / (per_launch_ms * 1e-3) / 1e12
     return {"bound": "fp32", "achieved": achieved, "peak": nominal, "unit": "TFLOP/s",
             "frac": achieved / nominal, "traffic": traffic, "kernel": dom,

@@ -190,9 +190,10 @@ void ente_profile_reset(void);
 int ente_profile_read(char *names, size_t names_len, int64_t *launches, double *ms,
                       int max_kernels);
 int ente_microbench_pce(int iters, int blocks, double *pce_per_s, void *stream);
-/* sub-tiles (32 candidates x 128 references) the two sweeps evaluated on the
- * current device since the last call (pruning skips the rest); synchronises */
-void ente_search_work(unsigned long long *knn_subtiles, unsigned long long *count_subtiles);
+/* (reference, candidate) pairs the two sweeps evaluated on the current device
+ * since the last call -- whole 32-candidate sub-tiles against a warp's
+ * reference group; pruning skips the rest; synchronises */
+void ente_search_work(unsigned long long *knn_pairs, unsigned long long *count_pairs);
 
 #ifdef __cplusplus
 }

@@ -228,7 +228,7 @@ def microbench_pce(iters: int = 200) -> float:
 
 
 def search_work() -> tuple[int, int]:
-    """(knn, count) sub-tiles evaluated since the last call (profiling on)."""
+    """(knn, count) reference-candidate pairs evaluated since the last call."""
     a, b = ctypes.c_ulonglong(), ctypes.c_ulonglong()
     lib().ente_search_work(ctypes.byref(a), ctypes.byref(b))
     return int(a.value), int(b.value)

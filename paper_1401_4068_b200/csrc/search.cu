@@ -101,44 +101,101 @@ __device__ int principal_axes(double (&cov)[kPcaCols][kPcaCols], int P, float (&
     return lead > 0.0 && (trace - top) < kPcaResidual * lead;
 }
 
-__global__ void __launch_bounds__(256) prep_kernel(const double *__restrict__ pts64, int dim,
-                                                   ChunkInfo *__restrict__ info,
-                                                   ColStats *__restrict__ stats,
-                                                   int32_t *__restrict__ status, int want32) {
+// One pass over the rows per group of 8 columns: fp64 sums / extrema, and
+// (first group) the fp32 covariance about the chunk's first row for the
+// principal axes.  The mean only centres the fp32 copy and enters the error
+// bound through max|x - m|, so its summation order is free.
+constexpr int kPrepThreads = 256;
+constexpr int kPrepWarps = kPrepThreads / 32;
+constexpr int kCovN = kPcaCols * (kPcaCols + 1) / 2;
+
+__global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double *__restrict__ pts64, int dim,
+                                                            ChunkInfo *__restrict__ info,
+                                                            ColStats *__restrict__ stats,
+                                                            int32_t *__restrict__ status, int want32) {
     const int c = blockIdx.x;
     const ChunkInfo ci = info[c];
     if (status[c] != ENTE_CHUNK_OK) return;
-    __shared__ double red[3][256];
+    __shared__ double wred[3][kPrepWarps][8];
+    __shared__ float wcov[kPrepWarps][kCovN];
     __shared__ ColStats local;
     __shared__ int bad;
     if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
     const double *p = pts64 + ci.row0 * dim;
-    ColStats *cs = &local;
-    for (int col = 0; col < dim; ++col) {
-        double s = 0.0, lo = INFINITY, hi = -INFINITY;
-        for (int r = threadIdx.x; r < ci.n; r += blockDim.x) {
-            const double v = p[(int64_t)r * dim + col];
-            s += v;
-            lo = fmin(lo, v);
-            hi = fmax(hi, v);
-            if (!isfinite(v)) bad = 1;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int P = dim < kPcaCols ? dim : kPcaCols;
+    for (int g0 = 0; g0 < dim; g0 += 8) {
+        const int gn = dim - g0 < 8 ? dim - g0 : 8;
+        double sum[8], lo[8], hi[8];
+        float cov[kCovN], x0[kPcaCols];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            sum[i] = 0.0;
+            lo[i] = INFINITY;
+            hi[i] = -INFINITY;
         }
-        red[0][threadIdx.x] = s;
-        red[1][threadIdx.x] = lo;
-        red[2][threadIdx.x] = hi;
-        __syncthreads();
-        for (int w = 128; w > 0; w >>= 1) {
-            if (threadIdx.x < w) {
-                red[0][threadIdx.x] += red[0][threadIdx.x + w];
-                red[1][threadIdx.x] = fmin(red[1][threadIdx.x], red[1][threadIdx.x + w]);
-                red[2][threadIdx.x] = fmax(red[2][threadIdx.x], red[2][threadIdx.x + w]);
+#pragma unroll
+        for (int e = 0; e < kCovN; ++e) cov[e] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < kPcaCols; ++i) x0[i] = (g0 == 0 && i < P) ? (float)p[i] : 0.0f;
+        int nonfinite = 0;
+        for (int r = threadIdx.x; r < ci.n; r += kPrepThreads) {
+            double v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = i < gn ? p[(int64_t)r * dim + g0 + i] : 0.0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                sum[i] += v[i];
+                lo[i] = fmin(lo[i], v[i]);
+                hi[i] = fmax(hi[i], v[i]);
+                nonfinite |= !isfinite(v[i]);
             }
-            __syncthreads();
+            if (g0 == 0 && stats) {
+                float x[kPcaCols];
+#pragma unroll
+                for (int i = 0; i < kPcaCols; ++i) x[i] = i < P ? (float)v[i] - x0[i] : 0.0f;
+                int e = 0;
+#pragma unroll
+                for (int i = 0; i < kPcaCols; ++i)
+#pragma unroll
+                    for (int j = 0; j <= i; ++j) cov[e++] += x[i] * x[j];
+            }
         }
-        if (threadIdx.x == 0) {
-            cs->mean[col] = red[0][0] / ci.n;
-            cs->lo[col] = red[1][0];
-            cs->hi[col] = red[2][0];
+        if (nonfinite) bad = 1;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            for (int off = 16; off > 0; off >>= 1) {
+                sum[i] += __shfl_xor_sync(0xffffffffu, sum[i], off);
+                lo[i] = fmin(lo[i], __shfl_xor_sync(0xffffffffu, lo[i], off));
+                hi[i] = fmax(hi[i], __shfl_xor_sync(0xffffffffu, hi[i], off));
+            }
+            if (lane == 0) {
+                wred[0][wid][i] = sum[i];
+                wred[1][wid][i] = lo[i];
+                wred[2][wid][i] = hi[i];
+            }
+        }
+        if (g0 == 0 && stats) {
+#pragma unroll
+            for (int e = 0; e < kCovN; ++e) {
+                float v = cov[e];
+                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                if (lane == 0) wcov[wid][e] = v;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < gn) {
+            const int i = threadIdx.x;
+            double sm = 0.0, l = INFINITY, h = -INFINITY;
+            for (int w = 0; w < kPrepWarps; ++w) {
+                sm += wred[0][w][i];
+                l = fmin(l, wred[1][w][i]);
+                h = fmax(h, wred[2][w][i]);
+            }
+            local.mean[g0 + i] = sm / ci.n;
+            local.lo[g0 + i] = l;
+            local.hi[g0 + i] = h;
         }
         __syncthreads();
     }
@@ -149,43 +206,21 @@ __global__ void __launch_bounds__(256) prep_kernel(const double *__restrict__ pt
         }
         return;
     }
+    const ColStats *cs = &local;
     if (stats) {
         for (int e = threadIdx.x; e < 3 * kMaxDim; e += blockDim.x)
             (&stats[c].mean[0])[e] = (&local.mean[0])[e];
-        // covariance of the first P columns -> two principal axes (kNN sort key)
-        const int P = dim < kPcaCols ? dim : kPcaCols;
-        __shared__ float wsum[8][kPcaCols * (kPcaCols + 1) / 2];
-        float acc[kPcaCols * (kPcaCols + 1) / 2];  // fp32: the axes only steer the order
-#pragma unroll
-        for (int e = 0; e < kPcaCols * (kPcaCols + 1) / 2; ++e) acc[e] = 0.0f;
-        for (int r = threadIdx.x; r < ci.n; r += blockDim.x) {
-            float x[kPcaCols];
-#pragma unroll
-            for (int i = 0; i < kPcaCols; ++i)
-                x[i] = i < P ? (float)(p[(int64_t)r * dim + i] - cs->mean[i]) : 0.0f;
-            int e = 0;
-#pragma unroll
-            for (int i = 0; i < kPcaCols; ++i)
-#pragma unroll
-                for (int j = 0; j <= i; ++j) acc[e++] += x[i] * x[j];
-        }
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-        for (int e = 0; e < kPcaCols * (kPcaCols + 1) / 2; ++e) {
-            float v = acc[e];
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-            if (lane == 0) wsum[wid][e] = v;
-        }
-        __syncthreads();
         if (threadIdx.x == 0) {
-            double cov[kPcaCols][kPcaCols];
+            // covariance about the mean from the moments about the first row
+            double cov[kPcaCols][kPcaCols], d[kPcaCols];
+            for (int i = 0; i < kPcaCols; ++i) d[i] = i < P ? cs->mean[i] - (double)(float)p[i] : 0.0;
             int e = 0;
             for (int i = 0; i < kPcaCols; ++i)
                 for (int j = 0; j <= i; ++j) {
                     double v = 0.0;
-                    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += wsum[w][e];
-                    cov[i][j] = cov[j][i] = v;
+                    for (int w = 0; w < kPrepWarps; ++w) v += wcov[w][e];
+                    v = v / ci.n - d[i] * d[j];
+                    cov[i][j] = cov[j][i] = (i < P && j < P) ? v : 0.0;
                     ++e;
                 }
             stats[c].use_pca = principal_axes(cov, P, stats[c].axis);
@@ -916,18 +951,19 @@ __global__ void __launch_bounds__(32, ENTE_CNT_MINB) count_pass_kernel(
             const float2 *c = reinterpret_cast<const float2 *>(cur);
             float a[kRT][2 * NP];
             float vA[kRT];
-            bool need = false;
+            bool need[kRT];
 #pragma unroll
             for (int r = 0; r < kRT; ++r) {
                 diff_pairs<D, 0, PG>(ref[r], c, a[r]);
                 vA[r] = maxabs0<1, 1 + DY, 2 * NP>(a[r]);
-                need |= vA[r] <= band[r].hi;
+                need[r] = vA[r] <= band[r].hi;
             }
-            if (!__any_sync(0xffffffffu, need)) continue;
-            float v2[kRT], v3[kRT], vj[kRT];
-            bool any = false;
+            // one warp vote per reference slot: the slots hold the two halves
+            // of the warp's Morton-ordered group, so a candidate often matters
+            // to one half only
 #pragma unroll
             for (int r = 0; r < kRT; ++r) {
+                if (!__any_sync(0xffffffffu, need[r])) continue;
                 diff_pairs<D, PG, NP>(ref[r], c, a[r]);
                 const float A = vA[r];
                 const float m2 = fmaxf(A, fabsf(a[r][0]));
@@ -943,23 +979,14 @@ __global__ void __launch_bounds__(32, ENTE_CNT_MINB) count_pass_kernel(
                 const float2 b1 = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nt, band[r].nt));
                 const float2 b2 = __fadd2_rn(make_float2(m3, jd), make_float2(band[r].nt, band[r].nt));
                 const float bm = fminf(fminf(fabsf(b1.x), fabsf(b1.y)), fminf(fabsf(b2.x), fabsf(b2.y)));
-                any |= bm <= band[r].w;
-                v2[r] = m2;
-                v3[r] = m3;
-                vj[r] = jd;
-            }
-            if (any) {
-                const int jg = cur_st * kSub + j;
-#pragma unroll
-                for (int r = 0; r < kRT; ++r) {
+                if (bm <= band[r].w) {
                     const float lo = band[r].lo, hi = band[r].hi;
-                    uint32_t f = ((vA[r] >= lo && vA[r] <= hi) ? 1u : 0u) |
-                                 ((v2[r] >= lo && v2[r] <= hi) ? 2u : 0u) |
-                                 ((v3[r] >= lo && v3[r] <= hi) ? 4u : 0u) |
-                                 ((vj[r] >= lo && vj[r] <= hi) ? 8u : 0u);
+                    uint32_t f = ((A >= lo && A <= hi) ? 1u : 0u) | ((m2 >= lo && m2 <= hi) ? 2u : 0u) |
+                                 ((m3 >= lo && m3 <= hi) ? 4u : 0u) | ((jd >= lo && jd <= hi) ? 8u : 0u);
                     f &= fmask;
                     if (f) {
                         const int idx = wrow + r * 32 + lane;
+                        const int jg = cur_st * kSub + j;
                         if (nev[r] < kCap) ev[(ci.row0 + idx) * kCap + nev[r]] = (uint32_t)jg | (f << 28);
                         ++nev[r];
                     }
@@ -1764,16 +1791,16 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
     return ENTE_OK;
 }
 
-// Evaluated 32-candidate x 128-reference sub-tiles of the two sweeps on the
+// Evaluated (reference, candidate) pairs (whole sub-tiles x reference groups) of the two sweeps on the
 // current device since the last call (synchronises the device): the pruned
 // work actually done.
-extern "C" void ente_search_work(unsigned long long *knn_subtiles, unsigned long long *count_subtiles) {
+extern "C" void ente_search_work(unsigned long long *knn_pairs, unsigned long long *count_pairs) {
     unsigned long long h[2] = {0, 0};
     unsigned long long *d = device_work();
     if (d && cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess)
         cudaMemset(d, 0, sizeof(h));
-    *knn_subtiles = h[0];
-    *count_subtiles = h[1];
+    *knn_pairs = h[0] * (unsigned long long)(kSub * kWarpRefs);
+    *count_pairs = h[1] * (unsigned long long)(kSub * kWarpRefs);
 }
 
 extern "C" size_t ente_radius_counts_workspace_size(int n_chunks) {
