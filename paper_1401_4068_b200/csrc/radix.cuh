@@ -1,6 +1,14 @@
 // CTA-wide stable LSD radix sort (8-bit digits) over global-memory ping-pong
-// buffers, one CTA per segment.  Used for the per-chunk spatial (Morton)
-// order of the sweeps and for numpy's ascending sort in the TE reduction.
+// buffers, one CTA per segment.  Used for the per-chunk spatial orders of the
+// sweeps and for numpy's ascending sort in the TE reduction.
+//
+// Each pass: a digit histogram (per-warp shared counters), then the segment
+// is scattered in tiles of kSortThreads * kSortItems keys held in registers.
+// Within a tile every warp ranks its 8 x 32 keys step by step with
+// __match_any_sync (stable: step-major, lane-minor order), the per-warp digit
+// counts are scanned across warps by one thread per digit, and every key goes
+// to running_offset[digit] + warp prefix + local rank.  Five CTA barriers per
+// tile of 4096 keys.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -8,12 +16,16 @@
 
 namespace ente {
 
-constexpr int kSortThreads = 256;
+constexpr int kSortThreads = 512;
 constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortItems = 8;  // keys per thread per tile
+constexpr int kSortTile = kSortThreads * kSortItems;
 
 struct SortSmem {
-    int hist[256];
-    int wcnt[kSortWarps][256];
+    int wcnt[kSortWarps][256];  // per-warp digit counts, then their exclusive scan
+    int off[256];               // running output offset of each digit
+    int tile_total[256];
+    int single;
 };
 
 // Sorts (keys, vals) of length n by the low `bits` bits of the keys.  The
@@ -28,48 +40,91 @@ __device__ int cta_radix_sort(K *ka, K *kb, V *va, V *vb, int n, int bits, SortS
     K *src = ka, *dst = kb;
     V *vsrc = va, *vdst = vb;
     for (int shift = 0; shift < bits; shift += 8) {
-        sm.hist[tid] = 0;
+        // ---- histogram
+        for (int e = tid; e < kSortWarps * 256; e += kSortThreads) (&sm.wcnt[0][0])[e] = 0;
+        if (tid == 0) sm.single = 0;
         __syncthreads();
-        for (int i = tid; i < n; i += kSortThreads) atomicAdd(&sm.hist[(int)((src[i] >> shift) & 255)], 1);
+        for (int i = tid; i < n; i += kSortThreads)
+            atomicAdd(&sm.wcnt[warp][(int)((src[i] >> shift) & 255)], 1);
         __syncthreads();
-        bool single = false;
-        for (int d = 0; d < 256; ++d) single |= sm.hist[d] == n;
+        if (tid < 256) {
+            int t = 0;
+            for (int w = 0; w < kSortWarps; ++w) t += sm.wcnt[w][tid];
+            sm.tile_total[tid] = t;
+            if (t == n) sm.single = 1;
+        }
         __syncthreads();
-        if (single) continue;
-        if (tid == 0) {
-            int run = 0;
-            for (int d = 0; d < 256; ++d) {
-                const int h = sm.hist[d];
-                sm.hist[d] = run;
-                run += h;
+        const int single = sm.single;
+        __syncthreads();
+        if (single) continue;  // uniform: every key shares this digit
+        if (tid < 32) {  // exclusive scan of the 256 digit totals by one warp
+            int v[8], s = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                v[q] = sm.tile_total[lane * 8 + q];
+                s += v[q];
+            }
+            int inc = s;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += u;
+            }
+            int run = inc - s;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                sm.off[lane * 8 + q] = run;
+                run += v[q];
             }
         }
         __syncthreads();
-        for (int base = 0; base < n; base += kSortThreads) {
-            const int i = base + tid;
-            const bool valid = i < n;
-            const K key = valid ? src[i] : K(0);
-            const int dig = valid ? (int)((key >> shift) & 255) : 256 + warp;
+        // ---- tiled scatter
+        for (int base = 0; base < n; base += kSortTile) {
+            for (int e = tid; e < kSortWarps * 256; e += kSortThreads) (&sm.wcnt[0][0])[e] = 0;
+            __syncthreads();
+            K key[kSortItems];
+            V val[kSortItems];
+            int dig[kSortItems], rank[kSortItems];
 #pragma unroll
-            for (int w = 0; w < kSortWarps; ++w) sm.wcnt[w][tid] = 0;
-            __syncthreads();
-            const unsigned peers = __match_any_sync(0xffffffffu, dig);
-            const int rank = __popc(peers & lt_mask);
-            if (valid && rank == 0) sm.wcnt[warp][dig] = __popc(peers);
-            __syncthreads();
-            if (valid) {
-                int pre = 0;
-                for (int w = 0; w < warp; ++w) pre += sm.wcnt[w][dig];
-                const int pos = sm.hist[dig] + pre + rank;
-                dst[pos] = key;
-                if (vsrc) vdst[pos] = vsrc[i];
+            for (int it = 0; it < kSortItems; ++it) {
+                const int i = base + warp * (32 * kSortItems) + it * 32 + lane;
+                const bool valid = i < n;
+                key[it] = valid ? src[i] : K(0);
+                if (vsrc) val[it] = valid ? vsrc[i] : V(0);
+                const int d = valid ? (int)((key[it] >> shift) & 255) : 256;
+                dig[it] = d;
+                const unsigned peers = __match_any_sync(0xffffffffu, d);
+                int before = 0;
+                if (valid) before = sm.wcnt[warp][d];
+                rank[it] = before + __popc(peers & lt_mask);
+                __syncwarp();
+                if (valid && (peers & lt_mask) == 0) sm.wcnt[warp][d] = before + __popc(peers);
+                __syncwarp();
             }
             __syncthreads();
-            int add = 0;
+            if (tid < 256) {  // scan the warps' counts of digit tid
+                int run = 0;
 #pragma unroll
-            for (int w = 0; w < kSortWarps; ++w) add += sm.wcnt[w][tid];
-            sm.hist[tid] += add;
+                for (int w = 0; w < kSortWarps; ++w) {
+                    const int c = sm.wcnt[w][tid];
+                    sm.wcnt[w][tid] = run;
+                    run += c;
+                }
+                sm.tile_total[tid] = run;
+            }
             __syncthreads();
+#pragma unroll
+            for (int it = 0; it < kSortItems; ++it) {
+                const int d = dig[it];
+                if (d < 256) {
+                    const int pos = sm.off[d] + sm.wcnt[warp][d] + rank[it];
+                    dst[pos] = key[it];
+                    if (vsrc) vdst[pos] = val[it];
+                }
+            }
+            __syncthreads();
+            if (tid < 256) sm.off[tid] += sm.tile_total[tid];
+            // (the next tile's zeroing barrier orders this update)
         }
         K *t = src;
         src = dst;

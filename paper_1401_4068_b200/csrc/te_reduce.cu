@@ -27,29 +27,106 @@ __device__ __forceinline__ double key_f64(uint64_t k) {
     return __longlong_as_double((long long)b);
 }
 
-__device__ double pairwise(const uint64_t *keys, int64_t n) {
+// numpy's pairwise_sum leaf (n <= 128): < 8 sequential, else eight
+// accumulators combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail
+__device__ double pairwise_leaf(const uint64_t *keys, int n) {
     if (n < 8) {
         double res = 0.0;
-        for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, key_f64(keys[i]));
+        for (int i = 0; i < n; ++i) res = __dadd_rn(res, key_f64(keys[i]));
         return res;
     }
-    if (n <= 128) {
-        double r[8];
+    double r[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = key_f64(keys[j]);
-        int64_t i = 8;
-        for (; i < n - (n % 8); i += 8) {
+    for (int j = 0; j < 8; ++j) r[j] = key_f64(keys[j]);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], key_f64(keys[i + j]));
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], key_f64(keys[i + j]));
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, key_f64(keys[i]));
+    return res;
+}
+
+// numpy's pairwise split: n > 128 -> (n2, n - n2), n2 = n/2 - (n/2) % 8
+__device__ __forceinline__ int pairwise_split(int n) {
+    int n2 = n / 2;
+    return n2 - n2 % 8;
+}
+
+// Parallel replica of numpy's pairwise sum over the sorted keys: thread 0
+// lists the leaves in depth-first order, all threads sum leaves, thread 0
+// folds the leaf sums back up the same tree.  `scratch` holds >= 8 n bytes.
+__device__ double pairwise_cta(const uint64_t *keys, int n, void *scratch, int *n_leaves) {
+    int2 *leaf = reinterpret_cast<int2 *>(scratch);  // (offset, length)
+    if (threadIdx.x == 0) {
+        int stack_off[40], stack_n[40], sp = 0, nl = 0;
+        stack_off[sp] = 0;
+        stack_n[sp++] = n;
+        while (sp) {
+            --sp;
+            const int off = stack_off[sp], m = stack_n[sp];
+            if (m <= 128) {
+                leaf[nl++] = make_int2(off, m);
+            } else {
+                const int m2 = pairwise_split(m);
+                stack_off[sp] = off + m2;  // right pushed first: left pops first
+                stack_n[sp++] = m - m2;
+                stack_off[sp] = off;
+                stack_n[sp++] = m2;
+            }
         }
-        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < n; ++i) res = __dadd_rn(res, key_f64(keys[i]));
-        return res;
+        *n_leaves = nl;
     }
-    int64_t n2 = n / 2;
-    n2 -= n2 % 8;
-    return __dadd_rn(pairwise(keys, n2), pairwise(keys + n2, n - n2));
+    __syncthreads();
+    const int nl = *n_leaves;
+    double *val = reinterpret_cast<double *>(leaf + nl);
+    for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+        const int2 d = leaf[l];
+        val[l] = pairwise_leaf(keys + d.x, d.y);
+    }
+    __syncthreads();
+    double res = 0.0;
+    if (threadIdx.x == 0) {
+        // post-order fold: the leaves come in DFS order, so a stack of
+        // (pending right subtree size, left value) replays the recursion
+        int st_n[40], st_state[40], sp = 0, next = 0;
+        double st_left[40];
+        double cur = 0.0;
+        st_n[sp] = n;
+        st_state[sp++] = 0;
+        bool have = false;
+        while (sp) {
+            const int top = sp - 1;
+            const int m = st_n[top];
+            if (m <= 128) {  // leaf: its value goes to the parent
+                cur = val[next++];
+                --sp;
+                have = true;
+            } else if (st_state[top] == 0) {  // descend left
+                st_state[top] = 1;
+                st_n[sp] = pairwise_split(m);
+                st_state[sp++] = 0;
+                have = false;
+                continue;
+            } else if (st_state[top] == 1) {  // left done: keep it, descend right
+                st_left[top] = cur;
+                st_state[top] = 2;
+                st_n[sp] = m - pairwise_split(m);
+                st_state[sp++] = 0;
+                have = false;
+                continue;
+            } else {  // both done
+                cur = __dadd_rn(st_left[top], cur);
+                --sp;
+                have = true;
+            }
+            (void)have;
+        }
+        res = cur;
+    }
+    return res;
 }
 
 struct RedChunk {
@@ -64,6 +141,7 @@ __global__ void __launch_bounds__(kSortThreads) te_reduce_kernel(
     uint64_t *__restrict__ kb, double *__restrict__ out_te) {
     __shared__ SortSmem sm;
     __shared__ int bad;
+    __shared__ int n_leaves;
     const RedChunk ch = chunks[blockIdx.x];
     const int n = ch.n;
     uint64_t *src = ka + ch.row0;
@@ -84,10 +162,8 @@ __global__ void __launch_bounds__(kSortThreads) te_reduce_kernel(
         return;
     }
     const int parity = cta_radix_sort<uint64_t, int>(src, dst, nullptr, nullptr, n, 64, sm);
-    if (threadIdx.x == 0) {
-        const double sum = pairwise(parity ? dst : src, n);
-        out_te[blockIdx.x] = __dadd_rn(psi_k, __ddiv_rn(sum, (double)n));
-    }
+    const double sum = pairwise_cta(parity ? dst : src, n, parity ? src : dst, &n_leaves);
+    if (threadIdx.x == 0) out_te[blockIdx.x] = __dadd_rn(psi_k, __ddiv_rn(sum, (double)n));
 }
 
 }  // namespace ente
