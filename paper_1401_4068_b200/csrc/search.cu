@@ -63,6 +63,8 @@ struct ColStats {
     double hi[kMaxDim];
     float axis[2][kPcaCols];  // the two leading principal axes (kNN order)
     int32_t use_pca;          // variance off the leading plane < kPcaResidual of lambda_1
+    float cov[kPcaCols * (kPcaCols + 1) / 2];  // moments about the first row (prep)
+    float x0[kPcaCols];                        // that row (fp32)
 };
 
 // The kNN pass sorts by the principal-axis Morton key only when the chunk is
@@ -70,6 +72,7 @@ struct ColStats {
 // Lorenz system: residual ~ 0.01); noise-driven AR data (residual >= 0.3)
 // keeps the y-past Morton order of the count pass.
 constexpr double kPcaResidual = 0.05;
+constexpr int kPcaMinRows = 4096;
 
 // Two leading eigenvectors of a symmetric P x P matrix by power iteration
 // with deflation (P <= 8; ordering quality only, not exactness).
@@ -89,8 +92,14 @@ __device__ int principal_axes(double (&cov)[kPcaCols][kPcaCols], int P, float (&
             }
             nrm = sqrt(nrm);
             if (!(nrm > 0.0)) break;
-            for (int i = 0; i < P; ++i) v[i] = w[i] / nrm;
+            double change = 0.0;
+            for (int i = 0; i < P; ++i) {
+                const double vi = w[i] / nrm;
+                change = fmax(change, fabs(vi - v[i]));
+                v[i] = vi;
+            }
             lam = nrm;
+            if (change < 1e-6) break;
         }
         for (int i = 0; i < kPcaCols; ++i) axis[a][i] = (i < P) ? (float)v[i] : 0.0f;
         for (int i = 0; i < P; ++i)
@@ -128,17 +137,12 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double *__rest
     for (int g0 = 0; g0 < dim; g0 += 8) {
         const int gn = dim - g0 < 8 ? dim - g0 : 8;
         double sum[8], lo[8], hi[8];
-        float cov[kCovN], x0[kPcaCols];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             sum[i] = 0.0;
             lo[i] = INFINITY;
             hi[i] = -INFINITY;
         }
-#pragma unroll
-        for (int e = 0; e < kCovN; ++e) cov[e] = 0.0f;
-#pragma unroll
-        for (int i = 0; i < kPcaCols; ++i) x0[i] = (g0 == 0 && i < P) ? (float)p[i] : 0.0f;
         int nonfinite = 0;
         for (int r = threadIdx.x; r < ci.n; r += kPrepThreads) {
             double v[8];
@@ -151,10 +155,19 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double *__rest
                 hi[i] = fmax(hi[i], v[i]);
                 nonfinite |= !isfinite(v[i]);
             }
-            if (g0 == 0 && stats) {
+        }
+        // second sweep over the (L2-resident) rows for the covariance, kept
+        // apart so that neither loop needs more than ~64 registers
+        float cov[kCovN], x0[kPcaCols];
+#pragma unroll
+        for (int e = 0; e < kCovN; ++e) cov[e] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < kPcaCols; ++i) x0[i] = (g0 == 0 && i < P) ? (float)p[i] : 0.0f;
+        if (g0 == 0 && stats && ci.n >= kPcaMinRows) {
+            for (int r = threadIdx.x; r < ci.n; r += kPrepThreads) {
                 float x[kPcaCols];
 #pragma unroll
-                for (int i = 0; i < kPcaCols; ++i) x[i] = i < P ? (float)v[i] - x0[i] : 0.0f;
+                for (int i = 0; i < kPcaCols; ++i) x[i] = i < P ? (float)p[(int64_t)r * dim + i] - x0[i] : 0.0f;
                 int e = 0;
 #pragma unroll
                 for (int i = 0; i < kPcaCols; ++i)
@@ -210,21 +223,12 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double *__rest
     if (stats) {
         for (int e = threadIdx.x; e < 3 * kMaxDim; e += blockDim.x)
             (&stats[c].mean[0])[e] = (&local.mean[0])[e];
-        if (threadIdx.x == 0) {
-            // covariance about the mean from the moments about the first row
-            double cov[kPcaCols][kPcaCols], d[kPcaCols];
-            for (int i = 0; i < kPcaCols; ++i) d[i] = i < P ? cs->mean[i] - (double)(float)p[i] : 0.0;
-            int e = 0;
-            for (int i = 0; i < kPcaCols; ++i)
-                for (int j = 0; j <= i; ++j) {
-                    double v = 0.0;
-                    for (int w = 0; w < kPrepWarps; ++w) v += wcov[w][e];
-                    v = v / ci.n - d[i] * d[j];
-                    cov[i][j] = cov[j][i] = (i < P && j < P) ? v : 0.0;
-                    ++e;
-                }
-            stats[c].use_pca = principal_axes(cov, P, stats[c].axis);
+        for (int e = threadIdx.x; e < kCovN; e += blockDim.x) {
+            float v = 0.0f;
+            for (int w = 0; w < kPrepWarps; ++w) v += wcov[w][e];
+            stats[c].cov[e] = v;
         }
+        if (threadIdx.x < kPcaCols) stats[c].x0[threadIdx.x] = threadIdx.x < P ? (float)p[threadIdx.x] : 0.0f;
     }
     if (threadIdx.x == 0 && stats) {
         // spread s = max |fl64(x - m)| is attained at a column extreme
@@ -238,6 +242,29 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double *__rest
         info[c].delta = 4.0 * 0x1p-24 * smax * (1.0 + 0x1p-20);
         info[c].ok32 = ok && want32;
     }
+}
+
+// principal axes of every chunk large enough to use them (one thread per
+// chunk; the serial power iteration stays out of the prep CTAs)
+__global__ void __launch_bounds__(128) axes_kernel(const ChunkInfo *__restrict__ info, int n_chunks,
+                                                   int dim, ColStats *__restrict__ stats) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_chunks) return;
+    const ChunkInfo ci = info[c];
+    ColStats &cs = stats[c];
+    cs.use_pca = 0;
+    if (!ci.ok32 || ci.n < kPcaMinRows) return;
+    const int P = dim < kPcaCols ? dim : kPcaCols;
+    // covariance about the mean from the moments about the first row
+    double cov[kPcaCols][kPcaCols], d[kPcaCols];
+    for (int i = 0; i < kPcaCols; ++i) d[i] = i < P ? cs.mean[i] - (double)cs.x0[i] : 0.0;
+    int e = 0;
+    for (int i = 0; i < kPcaCols; ++i)
+        for (int j = 0; j <= i; ++j) {
+            const double v = (double)cs.cov[e++] / ci.n - d[i] * d[j];
+            cov[i][j] = cov[j][i] = (i < P && j < P) ? v : 0.0;
+        }
+    cs.use_pca = principal_axes(cov, P, cs.axis);
 }
 
 // ---------------------------------------------------------------------------
@@ -1725,6 +1752,9 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
         }
         ENTE_LAUNCH("prep", st,
                     prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, w.stats, status, 1));
+        ENTE_CUDA(cudaGetLastError());
+        ENTE_LAUNCH("axes", st,
+                    axes_kernel<<<(n_chunks + 127) / 128, 128, 0, st>>>(w.info, n_chunks, dim, w.stats));
         ENTE_CUDA(cudaGetLastError());
         FilterCols sfc = p.fc;
         if (!prune) sfc.nf = 0;  // identity order

@@ -168,6 +168,9 @@ class PairPipeline:
         return (self.cfg.seed, u, 0 if perm_index < 0 else perm_index + 1)
 
     def _items(self, items) -> np.ndarray:
+        if isinstance(items, np.ndarray) and items.dtype == np.int32 and items.ndim == 2 \
+                and items.shape[1] == 3 and items.flags.c_contiguous:
+            return items
         it = np.asarray(items, dtype=np.int64)
         if it.ndim != 2 or it.shape[1] not in (2, 3):
             raise ValueError("items must be (u, perm_index) or (u, perm_index, t_lo) tuples")
@@ -189,9 +192,10 @@ class PairPipeline:
 
     def _states(self, it: np.ndarray) -> np.ndarray:
         """Jitter PCG64 states per item; seeds depend only on (u, perm), not the window."""
-        keys, inv = np.unique(it[:, :2], axis=0, return_inverse=True)
-        uniq = np.array([jitter_state(self.seed_tuple(int(u), int(p))) for u, p in keys],
-                        dtype=np.uint64)
+        key = (it[:, 0].astype(np.int64) << 32) | (it[:, 1].astype(np.int64) + 1)
+        keys, inv = np.unique(key, return_inverse=True)
+        uniq = np.array([jitter_state(self.seed_tuple(int(k >> 32), int(k & 0xFFFFFFFF) - 1))
+                         for k in keys.tolist()], dtype=np.uint64)
         return np.ascontiguousarray(uniq[inv.reshape(-1)])
 
     def _wave(self, it: np.ndarray) -> np.ndarray:
@@ -306,8 +310,12 @@ def analyze_windows(source: EnsembleSeries, target: EnsembleSeries, spec_x: Embe
     reps, s = target.n_repetitions, config.n_surrogates
     perms = [cached_permutation(config.seed, i, reps, config.strict_permutation) for i in range(s)]
     pipe.set_perms(perms)
-    per_win = [(u, -1) for u in us] + [(u, i) for u in grid for i in range(s)]
-    items = [(u, i, lo) for lo, _ in windows for (u, i) in per_win]
+    per_win = np.array([(u, -1) for u in us] + [(u, i) for u in grid for i in range(s)],
+                       dtype=np.int32).reshape(-1, 2)
+    starts = np.array([lo for lo, _ in windows], dtype=np.int32)
+    items = np.empty((len(starts) * len(per_win), 3), dtype=np.int32)  # window-major
+    items[:, :2] = np.tile(per_win, (len(starts), 1))
+    items[:, 2] = np.repeat(starts, len(per_win))
     te_all = pipe.run(items).reshape(len(windows), len(per_win))
     results = []
     for (lo, hi), row in zip(windows, te_all):

@@ -162,7 +162,11 @@ class Workload:
                                                       for i in range(s)]
         if self.window_starts is None:
             return per
-        return [(u, i, t) for t in self.window_starts for (u, i) in per]
+        starts = np.asarray(self.window_starts, dtype=np.int32)
+        arr = np.empty((len(starts) * len(per), 3), dtype=np.int32)  # window-major
+        arr[:, :2] = np.tile(np.asarray(per, dtype=np.int32), (len(starts), 1))
+        arr[:, 2] = np.repeat(starts, len(per))
+        return arr
 
     @property
     def chunk_points(self) -> int:
