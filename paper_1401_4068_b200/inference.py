@@ -145,7 +145,8 @@ class PairPipeline:
     estimate_te_batch calls would.
     """
 
-    def __init__(self, source, target, spec_x, spec_y, config: AnalysisConfig):
+    def __init__(self, source, target, spec_x, spec_y, config: AnalysisConfig,
+                 x_device=None, y_device=None):
         self.cfg = config
         self.sx, self.sy = spec_x, spec_y
         self.reps, self.n_samples = target.values.shape
@@ -154,8 +155,11 @@ class PairPipeline:
         self.m = self.reps * self.w
         self.dim = 1 + spec_y.dim + spec_x.dim
         dev = nat.device()
-        self.x = torch.from_numpy(np.array(source.values, dtype=np.float64)).to(dev)
-        self.y = torch.from_numpy(np.array(target.values, dtype=np.float64)).to(dev)
+        # x_device / y_device: the ensembles already in HBM (io_formats.load_ensemble_device)
+        self.x = x_device if x_device is not None else \
+            torch.from_numpy(np.array(source.values, dtype=np.float64)).to(dev)
+        self.y = y_device if y_device is not None else \
+            torch.from_numpy(np.array(target.values, dtype=np.float64)).to(dev)
         self.perm_dev = None
         self.perm_count = 0
 
@@ -220,8 +224,12 @@ class PairPipeline:
 
 def analyze_pair(source: EnsembleSeries, target: EnsembleSeries,
                  spec_x: EmbeddingSpec, spec_y: EmbeddingSpec,
-                 config: AnalysisConfig) -> TEResult:
-    """Delay scan + surrogate test for one directed pair in one window (TE in nats)."""
+                 config: AnalysisConfig, x_device=None, y_device=None) -> TEResult:
+    """Delay scan + surrogate test for one directed pair in one window (TE in nats).
+
+    x_device / y_device optionally pass the two ensembles already resident in
+    HBM (same values as source / target), skipping their upload.
+    """
     validate_ensemble(source)
     validate_ensemble(target)
     selected = config.scan_statistic == "selected"
@@ -235,7 +243,7 @@ def analyze_pair(source: EnsembleSeries, target: EnsembleSeries,
             assembly_error = exc
             us = us[:i]
             break
-    pipe = PairPipeline(source, target, spec_x, spec_y, config)
+    pipe = PairPipeline(source, target, spec_x, spec_y, config, x_device, y_device)
     reps = target.n_repetitions
     s = config.n_surrogates
     can_draw = reps >= 2 or not config.strict_permutation
