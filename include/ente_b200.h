@@ -87,6 +87,25 @@ int ente_search(const double *pts64, int64_t total_rows, int dim, const ente_chu
                void *stream);
 
 /* ---------------------------------------------------------------------------
+ * ente_knn_indices -- the k nearest neighbours of every point, in the
+ * canonical order ascending (fp64 max-norm distance, chunk-local index).
+ *
+ * No reference counterpart: ente.engine returns only kth_distance
+ * (engine.py:62-67, 170-176; SURVEY 8c "index parity unpinned"), so this
+ * order is the contract, pinned by an O(n^2) oracle (oracle/oracle.py
+ * knn_indices).  `eps` must be the exact kth distances of the same points
+ * (the out_eps of an ente_search call with the same chunks and k).
+ *
+ *   eps          [dev]  [total_rows] fp64
+ *   out_idx      [dev]  [total_rows x k] int32 chunk-local row indices
+ *   status       [dev]  [n_chunks] int32 (K_TOO_LARGE / NONFINITE as ente_search)
+ *   workspace           sized by ente_search_workspace_size(chunks, n, dim, 0, k)
+ * ------------------------------------------------------------------------- */
+int ente_knn_indices(const double *pts64, int64_t total_rows, int dim, const ente_chunk *chunks,
+                     int n_chunks, int k, const double *eps, int32_t *out_idx, int32_t *status,
+                     void *workspace, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
  * ente_radius_counts -- strict counts #{j != i : maxnorm_marg(p_i, p_j) < r_i}
  * for caller-given radii (fp64, exact), one count array per marginal.
  *

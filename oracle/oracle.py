@@ -98,6 +98,23 @@ def search(points, marginals, k, brute=False):
     return eps, [radius_counts(points, m, eps, brute) for m in marginals]
 
 
+def knn_indices(points, k):
+    """O(n^2) canonical k nearest neighbours: ascending (fp64 max-norm, index), self excluded.
+
+    The reference keeps only the k-th distance (engine.py:70-123); the index
+    order is this package's contract, stated by brute force."""
+    p = np.asarray(points, dtype=np.float64)
+    n = len(p)
+    out = np.empty((n, k), dtype=np.int64)
+    idx = np.arange(n)
+    for i in range(n):
+        d = np.abs(p - p[i]).max(axis=1)
+        d[i] = np.inf
+        order = np.lexsort((idx, d))  # primary d, then index
+        out[i] = order[:k]
+    return out
+
+
 def jittered_joint(joint, amplitude, seed):
     """ksg.py:52-59: joint + U(-1,1) * (amplitude * std(axis=0))."""
     out = np.array(joint, dtype=np.float64, copy=True)

@@ -1379,6 +1379,135 @@ __global__ void __launch_bounds__(kExactWarps * 32) exact_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// knn indices: the k nearest neighbours of every point in the canonical
+// order ascending (fp64 max-norm distance, chunk-local index) -- the
+// reference never returns them, so this order is the contract.
+// One warp per point; with the fp32 kNN-order copy the walk skips sub-tiles
+// whose all-column box lies beyond up(eps + delta) and compares d64 only for
+// candidates with d32 <= that bound (every j with d64 <= eps qualifies);
+// chunks without the fp32 copy are scanned in fp64.  Per-lane sorted
+// (d, j) lists of S >= k slots, k rounds of lexicographic warp minima.
+// ---------------------------------------------------------------------------
+constexpr int kIdxWarps = 4;
+
+__device__ __forceinline__ bool lex_less(double a, int ia, double b, int ib) {
+    return a < b || (a == b && ia < ib);
+}
+
+template <int DP, int S>
+__global__ void __launch_bounds__(kIdxWarps * 32) knn_index_kernel(
+    const double *__restrict__ pts64, int dim, const ChunkInfo *__restrict__ info, int n_chunks,
+    const int32_t *__restrict__ status, const float *__restrict__ pts32k,
+    const float *__restrict__ fboxk, const int32_t *__restrict__ permk,
+    const double *__restrict__ eps_in, int k, int64_t total_rows, int32_t *__restrict__ out_idx) {
+    constexpr int NB = 4 * kKnnQ;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * kIdxWarps;
+    for (int64_t it = (int64_t)blockIdx.x * kIdxWarps + (threadIdx.x >> 5); it < total_rows;
+         it += nwarps) {
+        const int c = chunk_of_row(info, n_chunks, it);
+        const ChunkInfo ci = info[c];
+        if (status[c] != ENTE_CHUNK_OK || it >= ci.row0 + ci.n) continue;
+        const bool use32 = ci.ok32 && pts32k;
+        // this warp's point: sorted position s (fp32 path) or local row
+        const int s = (int)(it - ci.row0);
+        const int local = use32 ? permk[it] : s;
+        const int64_t row = ci.row0 + local;
+        double r64[DP];
+#pragma unroll
+        for (int q = 0; q < DP; ++q) r64[q] = q < dim ? pts64[row * dim + q] : 0.0;
+        const double eps = eps_in[row];
+        double kd[S];
+        int kj[S];
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+            kd[q] = INFINITY;
+            kj[q] = 0x7FFFFFFF;
+        }
+        auto consider = [&](int j_local) {
+            const double *q64 = pts64 + (ci.row0 + j_local) * dim;
+            double d = 0.0;
+            for (int q = 0; q < dim; ++q) d = fmax(d, fabs(__dsub_rn(r64[q < DP ? q : 0], q64[q])));
+            if (d <= eps && lex_less(d, j_local, kd[S - 1], kj[S - 1])) {
+                int p = S - 1;
+                while (p > 0 && lex_less(d, j_local, kd[p - 1], kj[p - 1])) {
+                    kd[p] = kd[p - 1];
+                    kj[p] = kj[p - 1];
+                    --p;
+                }
+                kd[p] = d;
+                kj[p] = j_local;
+            }
+        };
+        if (use32) {
+            const float *cp = pts32k + ci.prow0 * DP;
+            const float4 *fb = reinterpret_cast<const float4 *>(fboxk) + (ci.prow0 / kSub) * 2 * kKnnQ;
+            const int nsub = ci.npad / kSub;
+            float ref[DP];
+#pragma unroll
+            for (int q = 0; q < DP; ++q) ref[q] = cp[(int64_t)s * DP + q];
+            const float hi = __double2float_ru(__dadd_ru(eps, ci.delta));
+            for (int base = 0; base < nsub; base += 32) {
+                const int st_l = base + lane;
+                bool need = false;
+                if (st_l < nsub) {
+                    const Box<kKnnQ> b = load_box<kKnnQ>(fb, st_l);
+                    float d = 0.0f;
+#pragma unroll
+                    for (int g = 0; g < NB; ++g) {
+                        const float4 l4 = b.lo[g >> 2], h4 = b.hi[g >> 2];
+                        const float l = (g & 3) == 0 ? l4.x : (g & 3) == 1 ? l4.y : (g & 3) == 2 ? l4.z : l4.w;
+                        const float h = (g & 3) == 0 ? h4.x : (g & 3) == 1 ? h4.y : (g & 3) == 2 ? h4.z : h4.w;
+                        if (g < dim) d = fmaxf(d, fmaxf(l - ref[g < DP ? g : 0], ref[g < DP ? g : 0] - h));
+                    }
+                    need = d <= hi;
+                }
+                uint32_t m = __ballot_sync(0xffffffffu, need);
+                while (m) {
+                    const int st = base + __ffs(m) - 1;
+                    m &= m - 1;
+                    const int j = st * kSub + lane;
+                    if (j >= ci.n || j == s) continue;
+                    const float *q32 = cp + (int64_t)j * DP;
+                    float d = 0.0f;
+#pragma unroll
+                    for (int q = 0; q < DP; ++q)
+                        if (q < dim) d = fmaxf(d, fabsf(q32[q] - ref[q]));
+                    if (d <= hi) consider(permk[ci.row0 + j]);
+                }
+            }
+        } else {
+            for (int j = lane; j < ci.n; j += 32)
+                if (j != local) consider(j);
+        }
+        // k rounds of the lexicographic warp minimum
+        for (int q = 0; q < k; ++q) {
+            double bd = kd[0];
+            int bj = kj[0];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double od = __shfl_xor_sync(0xffffffffu, bd, off);
+                const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
+                if (lex_less(od, oj, bd, bj)) {
+                    bd = od;
+                    bj = oj;
+                }
+            }
+            if (kj[0] == bj && kd[0] == bd) {  // the owner pops its head
+#pragma unroll
+                for (int p = 0; p < S - 1; ++p) {
+                    kd[p] = kd[p + 1];
+                    kj[p] = kj[p + 1];
+                }
+                kd[S - 1] = INFINITY;
+                kj[S - 1] = 0x7FFFFFFF;
+            }
+            if (lane == 0) out_idx[row * k + q] = bj;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host side: kernel tables and dispatch
 // ---------------------------------------------------------------------------
 using KnnFn = void (*)(const float *, const float *, const ChunkInfo *, const int32_t *, int, int,
@@ -1648,6 +1777,71 @@ static int validate(const ente_chunk *chunks, int n_chunks, int dim, const uint3
     return ENTE_OK;
 }
 
+// prep -> principal axes -> both sort orders -> both fp32 copies with boxes
+static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Plan &p,
+                         const SearchWs &w, int n_chunks, int32_t *status, int prune) {
+        ENTE_LAUNCH("prep", st,
+                    prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, w.stats, status, 1));
+        ENTE_CUDA(cudaGetLastError());
+        ENTE_LAUNCH("axes", st,
+                    axes_kernel<<<(n_chunks + 127) / 128, 128, 0, st>>>(w.info, n_chunks, dim, w.stats));
+        ENTE_CUDA(cudaGetLastError());
+        FilterCols sfc = p.fc;
+        if (!prune) sfc.nf = 0;  // identity order
+        ENTE_LAUNCH("sort", st,
+                    sort_kernel<<<n_chunks, kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats, sfc,
+                                                                   w.ka, w.kb, w.va, w.vb, w.perm));
+        ENTE_CUDA(cudaGetLastError());
+        ENTE_LAUNCH("sort_pca", st,
+                    sort_pca_kernel<<<n_chunks, kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats,
+                                                                       w.ka, w.kb, w.va, w.vb,
+                                                                       w.perm, w.permk));
+        ENTE_CUDA(cudaGetLastError());
+        dim3 ggrid((unsigned)(p.max_npad / kTJ), (unsigned)std::min(n_chunks, 65535));
+        ENTE_LAUNCH("gather", st,
+                    gather_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.stats,
+                                                         w.perm, p.dp, p.fc, w.pts32, w.fbox,
+                                                         w.inv));
+        ENTE_CUDA(cudaGetLastError());
+        ENTE_LAUNCH("gather_knn", st,
+                    gather_knn_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.stats,
+                                                             w.permk, w.inv, p.dp, w.pts32k,
+                                                             w.fboxk, w.kmap));
+        ENTE_CUDA(cudaGetLastError());
+    return ENTE_OK;
+}
+
+// host chunk table + status (K_TOO_LARGE) + per-chunk first sweep tile
+static int upload_chunks(cudaStream_t st, const ente_chunk *chunks, int n_chunks, int k,
+                         const Plan &p, const SearchWs &w, int32_t *status,
+                         std::vector<int32_t> &htile0, int32_t &ntiles) {
+    std::vector<ChunkInfo> hinfo(n_chunks);
+    std::vector<int32_t> hstatus(n_chunks, ENTE_CHUNK_OK);
+    htile0.assign(n_chunks + 1, 0);
+    ntiles = 0;
+    int64_t prow = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+        ChunkInfo &ci = hinfo[c];
+        ci.row0 = chunks[c].row0;
+        ci.n = chunks[c].n;
+        ci.npad = round_up(ci.n, kTJ);
+        ci.prow0 = prow;
+        ci.delta = 0.0;
+        ci.ok32 = 0;
+        prow += ci.npad;
+        if (k > ci.n - 1) hstatus[c] = ENTE_CHUNK_K_TOO_LARGE;
+        htile0[c] = ntiles;
+        if (p.fast && hstatus[c] == ENTE_CHUNK_OK) ntiles += (ci.n + kWarpRefs - 1) / kWarpRefs;
+    }
+    htile0[n_chunks] = ntiles;
+    ENTE_CUDA(cudaMemcpyAsync(w.info, hinfo.data(), sizeof(ChunkInfo) * n_chunks,
+                              cudaMemcpyHostToDevice, st));
+    ENTE_CUDA(cudaMemcpyAsync(status, hstatus.data(), sizeof(int32_t) * n_chunks,
+                              cudaMemcpyHostToDevice, st));
+    ENTE_CUDA(cudaMemsetAsync(w.ovf_n, 0, 2 * sizeof(int32_t), st));
+    return ENTE_OK;
+}
+
 }  // namespace ente
 
 using namespace ente;
@@ -1716,30 +1910,10 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
         return ENTE_ERR_WORKSPACE;
     }
     // host-side chunk table, tile list and k checks
-    std::vector<ChunkInfo> hinfo(n_chunks);
-    std::vector<int32_t> hstatus(n_chunks, ENTE_CHUNK_OK);
-    std::vector<int32_t> htile0(n_chunks + 1, 0);
+    std::vector<int32_t> htile0;
     int32_t ntiles = 0;
-    int64_t prow = 0;
-    for (int c = 0; c < n_chunks; ++c) {
-        ChunkInfo &ci = hinfo[c];
-        ci.row0 = chunks[c].row0;
-        ci.n = chunks[c].n;
-        ci.npad = round_up(ci.n, kTJ);
-        ci.prow0 = prow;
-        ci.delta = 0.0;
-        ci.ok32 = 0;
-        prow += ci.npad;
-        if (k > ci.n - 1) hstatus[c] = ENTE_CHUNK_K_TOO_LARGE;
-        htile0[c] = ntiles;
-        if (p.fast && hstatus[c] == ENTE_CHUNK_OK) ntiles += (ci.n + kWarpRefs - 1) / kWarpRefs;
-    }
-    htile0[n_chunks] = ntiles;
-    ENTE_CUDA(cudaMemcpyAsync(w.info, hinfo.data(), sizeof(ChunkInfo) * n_chunks,
-                              cudaMemcpyHostToDevice, st));
-    ENTE_CUDA(cudaMemcpyAsync(status, hstatus.data(), sizeof(int32_t) * n_chunks,
-                              cudaMemcpyHostToDevice, st));
-    ENTE_CUDA(cudaMemsetAsync(w.ovf_n, 0, 2 * sizeof(int32_t), st));
+    rc = upload_chunks(st, chunks, n_chunks, k, p, w, status, htile0, ntiles);
+    if (rc != ENTE_OK) return rc;
     Masks masks{};
     masks.n = n_marg;
     for (int m = 0; m < n_marg; ++m) masks.m[m] = marg_masks[m];
@@ -1750,34 +1924,8 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
             set_error("ente_search: cannot allocate the work counters");
             return ENTE_ERR_CUDA;
         }
-        ENTE_LAUNCH("prep", st,
-                    prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, w.stats, status, 1));
-        ENTE_CUDA(cudaGetLastError());
-        ENTE_LAUNCH("axes", st,
-                    axes_kernel<<<(n_chunks + 127) / 128, 128, 0, st>>>(w.info, n_chunks, dim, w.stats));
-        ENTE_CUDA(cudaGetLastError());
-        FilterCols sfc = p.fc;
-        if (!prune) sfc.nf = 0;  // identity order
-        ENTE_LAUNCH("sort", st,
-                    sort_kernel<<<n_chunks, kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats, sfc,
-                                                                   w.ka, w.kb, w.va, w.vb, w.perm));
-        ENTE_CUDA(cudaGetLastError());
-        ENTE_LAUNCH("sort_pca", st,
-                    sort_pca_kernel<<<n_chunks, kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats,
-                                                                       w.ka, w.kb, w.va, w.vb,
-                                                                       w.perm, w.permk));
-        ENTE_CUDA(cudaGetLastError());
-        dim3 ggrid((unsigned)(p.max_npad / kTJ), (unsigned)std::min(n_chunks, 65535));
-        ENTE_LAUNCH("gather", st,
-                    gather_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.stats,
-                                                         w.perm, p.dp, p.fc, w.pts32, w.fbox,
-                                                         w.inv));
-        ENTE_CUDA(cudaGetLastError());
-        ENTE_LAUNCH("gather_knn", st,
-                    gather_knn_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.stats,
-                                                             w.permk, w.inv, p.dp, w.pts32k,
-                                                             w.fboxk, w.kmap));
-        ENTE_CUDA(cudaGetLastError());
+        rc = launch_orders(st, pts64, dim, p, w, n_chunks, status, prune);
+        if (rc != ENTE_OK) return rc;
         ENTE_CUDA(cudaMemcpyAsync(w.tile0, htile0.data(), sizeof(int32_t) * (n_chunks + 1),
                                   cudaMemcpyHostToDevice, st));
         const unsigned nt = (unsigned)ntiles;
@@ -1831,6 +1979,66 @@ extern "C" void ente_search_work(unsigned long long *knn_pairs, unsigned long lo
         cudaMemset(d, 0, sizeof(h));
     *knn_pairs = h[0] * (unsigned long long)(kSub * kWarpRefs);
     *count_pairs = h[1] * (unsigned long long)(kSub * kWarpRefs);
+}
+
+
+extern "C" int ente_knn_indices(const double *pts64, int64_t total_rows, int dim,
+                                const ente_chunk *chunks, int n_chunks, int k,
+                                const double *eps, int32_t *out_idx, int32_t *status,
+                                void *workspace, size_t ws_bytes, void *stream) {
+    int rc = validate(chunks, n_chunks, dim, nullptr, 0, k);
+    if (rc != ENTE_OK) return rc;
+    if (n_chunks == 0) return ENTE_OK;
+    if (!eps || !out_idx) {
+        set_error("ente_knn_indices: eps and out_idx are required");
+        return ENTE_ERR_ARG;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint32_t none[kMaxMarg] = {0};
+    Plan p = make_plan(chunks, n_chunks, dim, none, 0, k);
+    if (p.total_rows > total_rows) {
+        set_error("ente_knn_indices: chunks reference row %lld beyond total_rows=%lld",
+                  (long long)p.total_rows, (long long)total_rows);
+        return ENTE_ERR_ARG;
+    }
+    Arena a(workspace, ws_bytes);
+    SearchWs w = layout_ws(a, p, n_chunks);
+    if (!a.ok() || !w.info) {
+        set_error("ente_knn_indices: workspace of %zu bytes too small (need %zu)", ws_bytes, a.used);
+        return ENTE_ERR_WORKSPACE;
+    }
+    std::vector<int32_t> htile0;
+    int32_t ntiles = 0;
+    rc = upload_chunks(st, chunks, n_chunks, k, p, w, status, htile0, ntiles);
+    if (rc != ENTE_OK) return rc;
+    if (p.fast && ntiles > 0) {
+        rc = launch_orders(st, pts64, dim, p, w, n_chunks, status, 1);
+        if (rc != ENTE_OK) return rc;
+    } else {
+        ENTE_LAUNCH("prep", st,
+                    prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, nullptr, status, 0));
+        ENTE_CUDA(cudaGetLastError());
+    }
+    const float *p32 = p.fast ? w.pts32k : nullptr;
+    const unsigned grid = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((p.total_rows + kIdxWarps - 1) / kIdxWarps, (int64_t)num_sms() * 64));
+    const int dp = (dim + 3) & ~3;
+    const int S = exact_slots(k);
+#define ENTE_IDX(DPV, SV)                                                                        \
+    if (dp == DPV && S == SV) {                                                                   \
+        ENTE_LAUNCH("knn_index", st,                                                              \
+                    knn_index_kernel<DPV, SV><<<grid, kIdxWarps * 32, 0, st>>>(                   \
+                        pts64, dim, w.info, n_chunks, status, p32, w.fboxk, w.permk, eps, k,     \
+                        p.total_rows, out_idx));                                                  \
+        ENTE_CUDA(cudaGetLastError());                                                           \
+        return ENTE_OK;                                                                           \
+    }
+#define ENTE_IDX_S(DPV) ENTE_IDX(DPV, 4) ENTE_IDX(DPV, 8) ENTE_IDX(DPV, 16) ENTE_IDX(DPV, 32) ENTE_IDX(DPV, 64)
+    ENTE_IDX_S(4) ENTE_IDX_S(8) ENTE_IDX_S(12) ENTE_IDX_S(16) ENTE_IDX_S(20)
+#undef ENTE_IDX_S
+#undef ENTE_IDX
+    set_error("ente_knn_indices: dim=%d is above the compiled maximum of 20", dim);
+    return ENTE_ERR_ARG;
 }
 
 extern "C" size_t ente_radius_counts_workspace_size(int n_chunks) {

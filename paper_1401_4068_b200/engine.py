@@ -211,6 +211,43 @@ def knn_kth_distances(chunk: Chunk, k: int) -> np.ndarray:
     return res.kth_distance
 
 
+def knn_indices_device(pts64: torch.Tensor, rows0, ns, k: int):
+    """(eps [rows] f64, idx [rows, k] int32, status) on the device: the k nearest
+    neighbours of every point, ascending (fp64 distance, chunk-local index)."""
+    rows, dim = pts64.shape
+    eps, _, status = search_device(pts64, rows0, ns, [], k)
+    L = nat.lib()
+    table = nat.chunk_table(rows0, ns)
+    idx = torch.empty((rows, k), dtype=torch.int32, device=pts64.device)
+    ws = nat.workspace(L.ente_search_workspace_size(table, len(ns), dim, 0, int(k)))
+    st2 = torch.empty_like(status)
+    nat.check(L.ente_knn_indices(nat.ptr(pts64), rows, dim, table, len(ns), int(k), nat.ptr(eps),
+                                 nat.ptr(idx), nat.ptr(st2), nat.ptr(ws), ws.numel(),
+                                 nat.stream_handle()), "ente_knn_indices")
+    return eps, idx, status
+
+
+def knn_indices(chunk: Chunk, k: int) -> np.ndarray:
+    """[n, k] int64 indices of each point's k nearest neighbours (self excluded).
+
+    Order: ascending max-norm distance, ties by ascending index -- the
+    canonical order the reference implies but never materialises (its
+    engine keeps only the k-th distance, engine.py:70-123).  Row i's k-th
+    entry is a neighbour at exactly knn_kth_distances(chunk, k)[i].
+    """
+    pts = chunk.points
+    n, dim = pts.shape
+    if k < 1 or k > n - 1:
+        raise KTooLarge(f"k={k} not in [1, n-1] for n={n}")
+    if dim > MAX_DIM or k > MAX_K:
+        raise NotImplementedError(f"dim={dim} (<= {MAX_DIM}) / k={k} (<= {MAX_K}) above the engine limits")
+    dev = _upload([pts])
+    _, idx, status = knn_indices_device(dev, [0], [n], k)
+    if int(status.cpu()[0]) == nat.CHUNK_NONFINITE:
+        raise ShapeMismatch("chunk contains non-finite values")
+    return idx.cpu().numpy().astype(np.int64)
+
+
 def radius_counts(chunk: Chunk, radii) -> np.ndarray:
     """#{j != i : maxnorm(p_i, p_j) < radii[i]} over all columns of the chunk."""
     radii = np.ascontiguousarray(np.asarray(radii, dtype=np.float64))

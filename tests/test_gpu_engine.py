@@ -192,3 +192,43 @@ def test_pruned_sweep_large_chunks(kind):
     assert np.array_equal(r.kth_distance, e)
     for a, b in zip(r.radius_counts, c):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("kind", ["random", "rounded", "duplicates", "lorenz_like", "lowdim"])
+@pytest.mark.parametrize("k", [1, 4, 9])
+def test_knn_indices_canonical_order(kind, k):
+    """Neighbour indices bit-exact vs the O(n^2) oracle: ascending (fp64 distance, index)."""
+    from paper_1401_4068_b200.engine import knn_indices
+    rng = np.random.default_rng(5 + k)
+    n = 1500
+    if kind == "random":
+        pts = rng.standard_normal((n, 7))
+    elif kind == "rounded":
+        pts = np.round(rng.standard_normal((n, 5)), 1)
+    elif kind == "duplicates":
+        pts = rng.standard_normal((n // 3, 3)).repeat(3, axis=0)
+    elif kind == "lorenz_like":
+        s = np.cumsum(rng.standard_normal(n + 10)) * 0.05
+        pts = np.stack([np.sin(s[i:i + n] * 0.7 + i) for i in range(7)], axis=1)
+    else:
+        pts = rng.standard_normal((n, 1))
+    got = knn_indices(Chunk(pts), k)
+    assert np.array_equal(got, oracle.knn_indices(pts, k))
+    # the k-th entry sits at exactly the k-th distance
+    eps = knn_kth_distances(Chunk(pts), k)
+    assert np.array_equal(np.abs(pts - pts[got[:, -1]]).max(axis=1), eps)
+
+
+def test_knn_indices_large_pruned_chunk():
+    from paper_1401_4068_b200.engine import knn_indices
+    rng = np.random.default_rng(2)
+    n = 12000
+    s = np.cumsum(rng.standard_normal(n + 10)) * 0.05
+    pts = np.stack([np.sin(s[i:i + n] * 0.7 + i) for i in range(7)], axis=1)
+    got = knn_indices(Chunk(pts), 4)
+    sel = rng.choice(n, 300, replace=False)
+    d = np.abs(pts[sel][:, None, :] - pts[None, :, :]).max(axis=2)
+    d[np.arange(300), sel] = np.inf
+    for row, i in enumerate(sel):
+        order = np.lexsort((np.arange(n), d[row]))[:4]
+        assert np.array_equal(got[i], order)
