@@ -661,6 +661,7 @@ struct Walker {
     int nst;        // per lane: sub-tile at position base + 32 + lane (prefetched)
     Box<Q> nb;      // its box
     Box<Q> own;     // the warp's own box, identical in all lanes
+    uint32_t need;  // per lane: refs_need() bits of the sub-tile last returned
 
     __device__ int sub_at(int pos) const {
         if (pos < nh) return h0 + pos;
@@ -726,7 +727,11 @@ struct Walker {
             const float d = __shfl_sync(0xffffffffu, wd, b);
             if (!(strict ? (d < bound) : (d <= bound))) continue;  // the bound may have shrunk
             const int st = __shfl_sync(0xffffffffu, wst, b);
-            if (__any_sync(0xffffffffu, refs_need(load_box<Q>(fb, st)))) return st;
+            const uint32_t nm = (uint32_t)refs_need(load_box<Q>(fb, st));
+            if (__any_sync(0xffffffffu, nm != 0u)) {
+                need = nm;
+                return st;
+            }
         }
     }
 };
@@ -894,8 +899,26 @@ __global__ void __launch_bounds__(32, ENTE_KNN_MINB) knn_pass_kernel(
 // pass 2: certain counts in the three TE marginals + band events
 //   marginal 0 = y-past (A), 1 = y + y-past (m2), 2 = y-past + x-past (m3)
 //   A <= every marginal and the joint, so A > hi settles a pair (outside
-//   everywhere, no event) after the gate columns alone
+//   everywhere, no event) after the gate columns alone.
+//
+// References are compacted.  The warp's 64 references live in
+// shared memory (coordinates, band, counts, event fill); for every streamed
+// sub-tile the walker's per-reference point-to-box tests say which of them
+// can have a pair inside the band (about a third of an evaluated sub-tile's
+// references), and only those are packed onto the lanes, one per lane, in
+// rounds of 32 -- most sub-tiles need one round instead of the two a fixed
+// two-references-per-lane mapping costs.  Per round a lane reloads its
+// reference from shared memory and folds its counts back afterwards.
 // ---------------------------------------------------------------------------
+template <int DP, int NSLOT>
+struct CountRefs {
+    float ref[32 * kRT][DP];  // fp32 centred coordinates
+    float lo[32 * kRT], hi[32 * kRT], t[32 * kRT], w[32 * kRT];
+    uint32_t cnt[3][32 * kRT];
+    int nev[32 * kRT];
+    int slot[32 * kRT];       // compacted reference list of the current sub-tile
+};
+
 template <int DY, int DX>
 __global__ void __launch_bounds__(32, ENTE_CNT_MINB) count_pass_kernel(
     const float *__restrict__ pts32, const float *__restrict__ fbox,
@@ -905,42 +928,53 @@ __global__ void __launch_bounds__(32, ENTE_CNT_MINB) count_pass_kernel(
     unsigned long long *__restrict__ work) {
     using L = Lay<DY, DX>;
     constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG, NSLOT = L::NSLOT;
+    constexpr int NR = 32 * kRT;
     __shared__ __align__(128) Ring<DP, NSLOT> ring;
+    __shared__ __align__(16) CountRefs<DP, NSLOT> rs;
     const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
     const int lane = threadIdx.x;
+    const unsigned lt = (1u << lane) - 1u;
     const float *cp = pts32 + ci.prow0 * DP;
     const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2;
     const int wrow = tr.r0;
-    float2 ref[kRT][NP];
-    Band band[kRT];
-    uint32_t cA[kRT], c2[kRT], c3[kRT];
-    int nev[kRT];
+    float2 myref[kRT][NP];  // this lane's own references (walker tests)
+    float myhi[kRT];
     float hmax = 0.0f;
 #pragma unroll
     for (int r = 0; r < kRT; ++r) {
-        const int idx = wrow + r * 32 + lane;
+        const int ri = r * 32 + lane;
+        const int idx = wrow + ri;
         const bool valid = idx < ci.n;
-        load_ref<D>(ref[r], cp + (int64_t)idx * DP, valid);
-        band[r] = make_band(valid ? t32_in[ci.row0 + idx] : 0.0f, ci.delta);
-        if (!valid) {  // empty band: never inside, never an event
-            band[r].lo = -INFINITY;
-            band[r].nlo = INFINITY;
-            band[r].hi = -INFINITY;
-            band[r].w = -1.0f;
+        load_ref<D>(myref[r], cp + (int64_t)idx * DP, valid);
+#pragma unroll
+        for (int c = 0; c < DP; ++c) rs.ref[ri][c] = (valid && c < D) ? cp[(int64_t)idx * DP + c] : 0.0f;
+        Band b = make_band(valid ? t32_in[ci.row0 + idx] : 0.0f, ci.delta);
+        if (!valid) {  // empty band: never inside, never an event, never needed
+            b.lo = -INFINITY;
+            b.hi = -INFINITY;
+            b.w = -1.0f;
+            b.nt = 0.0f;
         } else {
-            hmax = fmaxf(hmax, band[r].hi);
+            hmax = fmaxf(hmax, b.hi);
         }
-        cA[r] = c2[r] = c3[r] = 0;
-        nev[r] = 0;
+        rs.lo[ri] = b.lo;
+        rs.hi[ri] = b.hi;
+        rs.t[ri] = b.nt;
+        rs.w[ri] = b.w;
+        myhi[r] = b.hi;
+        rs.cnt[0][ri] = rs.cnt[1][ri] = rs.cnt[2][ri] = 0u;
+        rs.nev[ri] = 0;
     }
     const float bound = warp_max_nonneg(hmax);
     constexpr int NG = DY < kGate ? DY : kGate;
     auto refs_need = [&](const Box<1> &b) {
-        bool need = !prune;
+        uint32_t need = 0u;
 #pragma unroll
-        for (int r = 0; r < kRT; ++r) need |= point_box<1, NG, NP, 1>(ref[r], b) <= band[r].hi;
+        for (int r = 0; r < kRT; ++r)
+            need |= ((!prune && myhi[r] > -INFINITY) || point_box<1, NG, NP, 1>(myref[r], b) <= myhi[r])
+                        ? (1u << r) : 0u;
         return need;
     };
     if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
@@ -949,97 +983,122 @@ __global__ void __launch_bounds__(32, ENTE_CNT_MINB) count_pass_kernel(
     Walker<1> wk;
     wk.init(fb, wrow, ci.n, ci.npad);
     int slot_st = -1;
+    uint32_t slot_need = 0u;  // kRT bits per ring slot: this lane's needs of the issued sub-tiles
     int issued = 0;
     uint32_t nsub = 0;
     for (; issued < NSLOT; ++issued) {
         const int st = wk.next(fb, prune ? bound : INFINITY, false, refs_need);
         if (st < 0) break;
         if (lane == issued) slot_st = st;
+        slot_need |= wk.need << (kRT * issued);
         if (lane == 0) ring_issue(ring, issued, cp + (int64_t)st * kSub * DP);
     }
     for (int used = 0; used < issued; ++used) {
         const int slot = used % NSLOT;
         const int cur_st = __shfl_sync(0xffffffffu, slot_st, slot);
+        const uint32_t nb = (slot_need >> (kRT * slot)) & ((1u << kRT) - 1u);
+        // compact the references that need this sub-tile
+        int base = 0;
+#pragma unroll
+        for (int r = 0; r < kRT; ++r) {
+            const uint32_t m = __ballot_sync(0xffffffffu, (nb >> r) & 1u);
+            if ((nb >> r) & 1u) rs.slot[base + __popc(m & lt)] = r * 32 + lane;
+            base += __popc(m);
+        }
+        const int nneed = base;
+        __syncwarp();
         mbar_wait(&ring.full[slot], (uint32_t)(used / NSLOT) & 1u);
         const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[slot]);
         constexpr int NQ = DP / 4;
-        float4 nxt[NQ];
+        for (int round = 0; round < nneed; round += 32) {
+            const bool active = round + lane < nneed;
+            const int ri = active ? rs.slot[round + lane] : 0;
+            float2 ref[NP];
+            {
+                const float2 *rr = reinterpret_cast<const float2 *>(rs.ref[ri]);
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) nxt[q] = tile[q];
+                for (int p = 0; p < NP; ++p) {
+                    const float2 v = rr[p];
+                    ref[p] = make_float2(-v.x, -v.y);
+                }
+            }
+            const float lo = active ? rs.lo[ri] : -INFINITY;
+            const float hi = active ? rs.hi[ri] : -INFINITY;
+            const float nlo = -lo, nt = rs.t[ri], wb = active ? rs.w[ri] : -1.0f;
+            uint32_t cA = 0u, c2 = 0u, c3 = 0u;
+            int nev = active ? rs.nev[ri] : 0;
+            const int64_t evrow = (ci.row0 + wrow + ri) * kCap;
+            float4 nxt[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) nxt[q] = tile[q];
 #pragma unroll 2
-        for (int j = 0; j < kSub; ++j) {
-            float4 cur[NQ];
+            for (int j = 0; j < kSub; ++j) {
+                float4 cur[NQ];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) cur[q] = nxt[q];
-            if (j + 1 < kSub) {  // prefetch the next candidate row
+                for (int q = 0; q < NQ; ++q) cur[q] = nxt[q];
+                if (j + 1 < kSub) {
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) nxt[q] = tile[(j + 1) * NQ + q];
-            }
-            const float2 *c = reinterpret_cast<const float2 *>(cur);
-            float a[kRT][2 * NP];
-            float vA[kRT];
-            bool need[kRT];
-#pragma unroll
-            for (int r = 0; r < kRT; ++r) {
-                diff_pairs<D, 0, PG>(ref[r], c, a[r]);
-                vA[r] = maxabs0<1, 1 + DY, 2 * NP>(a[r]);
-                need[r] = vA[r] <= band[r].hi;
-            }
-            // one warp vote per reference slot: the slots hold the two halves
-            // of the warp's Morton-ordered group, so a candidate often matters
-            // to one half only
-#pragma unroll
-            for (int r = 0; r < kRT; ++r) {
-                if (!__any_sync(0xffffffffu, need[r])) continue;
-                diff_pairs<D, PG, NP>(ref[r], c, a[r]);
-                const float A = vA[r];
-                const float m2 = fmaxf(A, fabsf(a[r][0]));
-                const float m3 = maxabs<1 + DY, D, 2 * NP>(a[r], A);
+                    for (int q = 0; q < NQ; ++q) nxt[q] = tile[(j + 1) * NQ + q];
+                }
+                const float2 *c = reinterpret_cast<const float2 *>(cur);
+                float a[2 * NP];
+                diff_pairs<D, 0, PG>(ref, c, a);
+                const float A = maxabs0<1, 1 + DY, 2 * NP>(a);
+                if (!__any_sync(0xffffffffu, A <= hi)) continue;
+                diff_pairs<D, PG, NP>(ref, c, a);
+                const float m2 = fmaxf(A, fabsf(a[0]));
+                const float m3 = maxabs<1 + DY, D, 2 * NP>(a, A);
                 const float jd = fmaxf(m2, m3);
-                // certain-inside counts: sign bit of (v - lo)
-                const float2 e = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nlo, band[r].nlo));
-                const float e3 = m3 + band[r].nlo;
-                cA[r] += __float_as_uint(e.x) >> 31;
-                c2[r] += __float_as_uint(e.y) >> 31;
-                c3[r] += __float_as_uint(e3) >> 31;
-                // conservative band test: min |v - t| <= w
-                const float2 b1 = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nt, band[r].nt));
-                const float2 b2 = __fadd2_rn(make_float2(m3, jd), make_float2(band[r].nt, band[r].nt));
+                const float2 e = __fadd2_rn(make_float2(A, m2), make_float2(nlo, nlo));
+                const float e3 = m3 + nlo;
+                cA += __float_as_uint(e.x) >> 31;
+                c2 += __float_as_uint(e.y) >> 31;
+                c3 += __float_as_uint(e3) >> 31;
+                const float2 b1 = __fadd2_rn(make_float2(A, m2), make_float2(nt, nt));
+                const float2 b2 = __fadd2_rn(make_float2(m3, jd), make_float2(nt, nt));
                 const float bm = fminf(fminf(fabsf(b1.x), fabsf(b1.y)), fminf(fabsf(b2.x), fabsf(b2.y)));
-                if (bm <= band[r].w) {
-                    const float lo = band[r].lo, hi = band[r].hi;
+                if (bm <= wb) {
                     uint32_t f = ((A >= lo && A <= hi) ? 1u : 0u) | ((m2 >= lo && m2 <= hi) ? 2u : 0u) |
                                  ((m3 >= lo && m3 <= hi) ? 4u : 0u) | ((jd >= lo && jd <= hi) ? 8u : 0u);
                     f &= fmask;
                     if (f) {
-                        const int idx = wrow + r * 32 + lane;
-                        const int jg = cur_st * kSub + j;
-                        if (nev[r] < kCap) ev[(ci.row0 + idx) * kCap + nev[r]] = (uint32_t)jg | (f << 28);
-                        ++nev[r];
+                        if (nev < kCap) ev[evrow + nev] = (uint32_t)(cur_st * kSub + j) | (f << 28);
+                        ++nev;
                     }
                 }
             }
+            if (active) {
+                rs.cnt[0][ri] += cA;
+                rs.cnt[1][ri] += c2;
+                rs.cnt[2][ri] += c3;
+                rs.nev[ri] = nev;
+            }
+            __syncwarp();
         }
         ++nsub;
         __syncwarp();
         const int st = wk.next(fb, prune ? bound : INFINITY, false, refs_need);
         if (st >= 0) {
-            if (lane == issued % NSLOT) slot_st = st;
-            if (lane == 0) ring_issue(ring, issued % NSLOT, cp + (int64_t)st * kSub * DP);
+            const int ns = issued % NSLOT;
+            if (lane == ns) slot_st = st;
+            slot_need = (slot_need & ~(((1u << kRT) - 1u) << (kRT * ns))) | (wk.need << (kRT * ns));
+            if (lane == 0) ring_issue(ring, ns, cp + (int64_t)st * kSub * DP);
             ++issued;
         }
     }
     if (lane == 0) atomicAdd(work, (unsigned long long)nsub);
+    __syncwarp();
 #pragma unroll
     for (int r = 0; r < kRT; ++r) {
-        const int idx = wrow + r * 32 + lane;
+        const int ri = r * 32 + lane;
+        const int idx = wrow + ri;
         if (idx >= ci.n) continue;
-        const uint32_t self = band[r].lo > 0.0f ? 1u : 0u;  // the self pair counted as inside
+        const uint32_t self = rs.lo[ri] > 0.0f ? 1u : 0u;  // the self pair counted as inside
         const int64_t row = ci.row0 + idx;
-        cnt_out[row] = (int32_t)(cA[r] - self);
-        cnt_out[ws_rows + row] = (int32_t)(c2[r] - self);
-        cnt_out[2 * ws_rows + row] = (int32_t)(c3[r] - self);
-        ev_n[row] = nev[r];
+        cnt_out[row] = (int32_t)(rs.cnt[0][ri] - self);
+        cnt_out[ws_rows + row] = (int32_t)(rs.cnt[1][ri] - self);
+        cnt_out[2 * ws_rows + row] = (int32_t)(rs.cnt[2][ri] - self);
+        ev_n[row] = rs.nev[ri];
     }
 }
 
