@@ -90,34 +90,52 @@ __global__ void __launch_bounds__(32) jitter_std_kernel(const double *__restrict
     half_width[(int64_t)blockIdx.x * kMaxDim + col] = __dmul_rn(amplitude, sd);
 }
 
+// Element e of a chunk (C order) takes the PCG64 output after step e + 1.
+// Threads own elements e0 + t + kJitThreads * i (coalesced); each advances
+// its state by kJitThreads steps with one precomputed affine LCG jump.
+constexpr int kJitThreads = 256;
 constexpr int kJitPerThread = 64;
 
-__global__ void __launch_bounds__(256) jitter_apply_kernel(double *__restrict__ pts, int dim,
-                                                           const JitChunk *__restrict__ ch,
-                                                           const double *__restrict__ half_width,
-                                                           int n_chunks) {
+__global__ void __launch_bounds__(kJitThreads) jitter_apply_kernel(double *__restrict__ pts, int dim,
+                                                                   const JitChunk *__restrict__ ch,
+                                                                   const double *__restrict__ half_width,
+                                                                   int n_chunks) {
     for (int ci = blockIdx.y; ci < n_chunks; ci += gridDim.y) {  // grid.y <= 65535
-    const JitChunk c = ch[ci];
-    const int64_t total = (int64_t)c.n * dim;
-    const int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kJitPerThread;
-    if (e0 >= total) continue;
-    const int64_t e1 = e0 + kJitPerThread < total ? e0 + kJitPerThread : total;
-    U128 s = pcg_advance(c.state, c.inc, (uint64_t)e0);
-    double *p = pts + c.row0 * dim;
-    const double *hw = half_width + (int64_t)ci * kMaxDim;
-    int col = (int)(e0 % dim);
-    for (int64_t e = e0; e < e1; ++e) {
-        s = add128(mul128(s, kPcgMult), c.inc);
-        const uint64_t raw = pcg_output(s);
-        const double u01 = (double)(raw >> 11) * 0x1p-53;
-        const double u = __dadd_rn(-1.0, 2.0 * u01);
-        p[e] = __dadd_rn(p[e], __dmul_rn(u, hw[col]));
-        if (++col == dim) col = 0;
-    }
+        const JitChunk c = ch[ci];
+        const int64_t total = (int64_t)c.n * dim;
+        const int64_t base = (int64_t)blockIdx.x * kJitThreads * kJitPerThread;
+        if (base >= total) continue;
+        int64_t e = base + threadIdx.x;
+        // jump of kJitThreads steps: s' = A s + C
+        U128 A = {0ull, 1ull}, C = {0ull, 0ull};
+        {
+            U128 m = kPcgMult, plus = c.inc;
+            uint64_t d = kJitThreads;
+            while (d) {
+                if (d & 1ull) {
+                    A = mul128(A, m);
+                    C = add128(mul128(C, m), plus);
+                }
+                plus = mul128(add128(m, U128{0ull, 1ull}), plus);
+                m = mul128(m, m);
+                d >>= 1;
+            }
+        }
+        U128 s = pcg_advance(c.state, c.inc, (uint64_t)e + 1);  // state after step e + 1
+        double *p = pts + c.row0 * dim;
+        const double *hw = half_width + (int64_t)ci * kMaxDim;
+        for (int i = 0; i < kJitPerThread && e < total; ++i, e += kJitThreads) {
+            const uint64_t raw = pcg_output(s);
+            const double u01 = (double)(raw >> 11) * 0x1p-53;
+            const double u = __dadd_rn(-1.0, 2.0 * u01);
+            p[e] = __dadd_rn(p[e], __dmul_rn(u, hw[(int)(e % dim)]));
+            s = add128(mul128(A, s), C);
+        }
     }
 }
 
-// status: non-finite beats degenerate (np.ptp of a NaN column is NaN != 0)
+// status: non-finite beats degenerate (np.ptp of a NaN column is NaN != 0);
+// one pass over the rows, per-thread column extrema (dim <= kMaxDim)
 __global__ void __launch_bounds__(256) check_kernel(const double *__restrict__ pts, int dim,
                                                     const JitChunk *__restrict__ ch,
                                                     int32_t *__restrict__ status) {
@@ -129,21 +147,35 @@ __global__ void __launch_bounds__(256) check_kernel(const double *__restrict__ p
     const double *p = pts + c.row0 * dim;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int lbad = 0;
-    for (int q = 0; q < dim; ++q) {
-        double a = INFINITY, b = -INFINITY;
+    for (int g0 = 0; g0 < dim; g0 += 8) {
+        const int gn = dim - g0 < 8 ? dim - g0 : 8;
+        double a[8], b[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            a[i] = INFINITY;
+            b[i] = -INFINITY;
+        }
         for (int r = threadIdx.x; r < c.n; r += blockDim.x) {
-            const double v = p[(int64_t)r * dim + q];
-            lbad |= !isfinite(v);
-            a = fmin(a, v);
-            b = fmax(b, v);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (i < gn) {
+                    const double v = p[(int64_t)r * dim + g0 + i];
+                    lbad |= !isfinite(v);
+                    a[i] = fmin(a[i], v);
+                    b[i] = fmax(b[i], v);
+                }
+            }
         }
-        for (int off = 16; off > 0; off >>= 1) {
-            a = fmin(a, __shfl_xor_sync(0xffffffffu, a, off));
-            b = fmax(b, __shfl_xor_sync(0xffffffffu, b, off));
-        }
-        if (lane == 0) {
-            wmin[warp][q] = a;
-            wmax[warp][q] = b;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            for (int off = 16; off > 0; off >>= 1) {
+                a[i] = fmin(a[i], __shfl_xor_sync(0xffffffffu, a[i], off));
+                b[i] = fmax(b[i], __shfl_xor_sync(0xffffffffu, b[i], off));
+            }
+            if (lane == 0 && i < gn) {
+                wmin[warp][g0 + i] = a[i];
+                wmax[warp][g0 + i] = b[i];
+            }
         }
     }
     if (lbad) bad = 1;
@@ -230,11 +262,12 @@ extern "C" int ente_jitter(double *pts64, int dim, const ente_chunk *chunks, int
         ENTE_LAUNCH("jitter_std", st,
                     jitter_std_kernel<<<n_chunks, 32, 0, st>>>(pts64, dim, w.ch, amplitude, w.hw));
         ENTE_CUDA(cudaGetLastError());
-        const int64_t per_block = 256LL * kJitPerThread;
+        const int64_t per_block = (int64_t)kJitThreads * kJitPerThread;
         const int64_t gx = ((int64_t)max_n * dim + per_block - 1) / per_block;
         dim3 grid((unsigned)gx, (unsigned)(n_chunks < 65535 ? n_chunks : 65535));
         ENTE_LAUNCH("jitter_apply", st,
-                    jitter_apply_kernel<<<grid, 256, 0, st>>>(pts64, dim, w.ch, w.hw, n_chunks));
+                    jitter_apply_kernel<<<grid, kJitThreads, 0, st>>>(pts64, dim, w.ch, w.hw,
+                                                                      n_chunks));
         ENTE_CUDA(cudaGetLastError());
     }
     ENTE_LAUNCH("check", st, check_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.ch, status));

@@ -896,6 +896,159 @@ __global__ void __launch_bounds__(32, ENTE_KNN_MINB) knn_pass_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// pass 2, direct mapping (small chunks): two fixed references per lane
+//   marginal 0 = y-past (A), 1 = y + y-past (m2), 2 = y-past + x-past (m3)
+//   A <= every marginal and the joint, so A > hi settles a pair (outside
+//   everywhere, no event) after the gate columns alone
+// ---------------------------------------------------------------------------
+template <int DY, int DX>
+__global__ void __launch_bounds__(32, ENTE_CNT_MINB) count_pass_direct_kernel(
+    const float *__restrict__ pts32, const float *__restrict__ fbox,
+    const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks,
+    const float *__restrict__ t32_in, int64_t ws_rows, int prune, int32_t *__restrict__ cnt_out,
+    uint32_t *__restrict__ ev, int32_t *__restrict__ ev_n, uint32_t fmask,
+    unsigned long long *__restrict__ work) {
+    using L = Lay<DY, DX>;
+    constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG, NSLOT = L::NSLOT;
+    __shared__ __align__(128) Ring<DP, NSLOT> ring;
+    const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
+    const ChunkInfo ci = info[tr.chunk];
+    if (!ci.ok32) return;
+    const int lane = threadIdx.x;
+    const float *cp = pts32 + ci.prow0 * DP;
+    const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2;
+    const int wrow = tr.r0;
+    float2 ref[kRT][NP];
+    Band band[kRT];
+    uint32_t cA[kRT], c2[kRT], c3[kRT];
+    int nev[kRT];
+    float hmax = 0.0f;
+#pragma unroll
+    for (int r = 0; r < kRT; ++r) {
+        const int idx = wrow + r * 32 + lane;
+        const bool valid = idx < ci.n;
+        load_ref<D>(ref[r], cp + (int64_t)idx * DP, valid);
+        band[r] = make_band(valid ? t32_in[ci.row0 + idx] : 0.0f, ci.delta);
+        if (!valid) {  // empty band: never inside, never an event
+            band[r].lo = -INFINITY;
+            band[r].nlo = INFINITY;
+            band[r].hi = -INFINITY;
+            band[r].w = -1.0f;
+        } else {
+            hmax = fmaxf(hmax, band[r].hi);
+        }
+        cA[r] = c2[r] = c3[r] = 0;
+        nev[r] = 0;
+    }
+    const float bound = warp_max_nonneg(hmax);
+    constexpr int NG = DY < kGate ? DY : kGate;
+    auto refs_need = [&](const Box<1> &b) {
+        bool need = !prune;
+#pragma unroll
+        for (int r = 0; r < kRT; ++r) need |= point_box<1, NG, NP, 1>(ref[r], b) <= band[r].hi;
+        return need;
+    };
+    if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
+    fence_barrier_init();
+    __syncwarp();
+    Walker<1> wk;
+    wk.init(fb, wrow, ci.n, ci.npad);
+    int slot_st = -1;
+    int issued = 0;
+    uint32_t nsub = 0;
+    for (; issued < NSLOT; ++issued) {
+        const int st = wk.next(fb, prune ? bound : INFINITY, false, refs_need);
+        if (st < 0) break;
+        if (lane == issued) slot_st = st;
+        if (lane == 0) ring_issue(ring, issued, cp + (int64_t)st * kSub * DP);
+    }
+    for (int used = 0; used < issued; ++used) {
+        const int slot = used % NSLOT;
+        const int cur_st = __shfl_sync(0xffffffffu, slot_st, slot);
+        mbar_wait(&ring.full[slot], (uint32_t)(used / NSLOT) & 1u);
+        const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[slot]);
+        constexpr int NQ = DP / 4;
+        float4 nxt[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) nxt[q] = tile[q];
+#pragma unroll 2
+        for (int j = 0; j < kSub; ++j) {
+            float4 cur[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) cur[q] = nxt[q];
+            if (j + 1 < kSub) {  // prefetch the next candidate row
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) nxt[q] = tile[(j + 1) * NQ + q];
+            }
+            const float2 *c = reinterpret_cast<const float2 *>(cur);
+            float a[kRT][2 * NP];
+            float vA[kRT];
+            bool need[kRT];
+#pragma unroll
+            for (int r = 0; r < kRT; ++r) {
+                diff_pairs<D, 0, PG>(ref[r], c, a[r]);
+                vA[r] = maxabs0<1, 1 + DY, 2 * NP>(a[r]);
+                need[r] = vA[r] <= band[r].hi;
+            }
+            // one warp vote per reference slot: the slots hold the two halves
+            // of the warp's Morton-ordered group, so a candidate often matters
+            // to one half only
+#pragma unroll
+            for (int r = 0; r < kRT; ++r) {
+                if (!__any_sync(0xffffffffu, need[r])) continue;
+                diff_pairs<D, PG, NP>(ref[r], c, a[r]);
+                const float A = vA[r];
+                const float m2 = fmaxf(A, fabsf(a[r][0]));
+                const float m3 = maxabs<1 + DY, D, 2 * NP>(a[r], A);
+                const float jd = fmaxf(m2, m3);
+                // certain-inside counts: sign bit of (v - lo)
+                const float2 e = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nlo, band[r].nlo));
+                const float e3 = m3 + band[r].nlo;
+                cA[r] += __float_as_uint(e.x) >> 31;
+                c2[r] += __float_as_uint(e.y) >> 31;
+                c3[r] += __float_as_uint(e3) >> 31;
+                // conservative band test: min |v - t| <= w
+                const float2 b1 = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nt, band[r].nt));
+                const float2 b2 = __fadd2_rn(make_float2(m3, jd), make_float2(band[r].nt, band[r].nt));
+                const float bm = fminf(fminf(fabsf(b1.x), fabsf(b1.y)), fminf(fabsf(b2.x), fabsf(b2.y)));
+                if (bm <= band[r].w) {
+                    const float lo = band[r].lo, hi = band[r].hi;
+                    uint32_t f = ((A >= lo && A <= hi) ? 1u : 0u) | ((m2 >= lo && m2 <= hi) ? 2u : 0u) |
+                                 ((m3 >= lo && m3 <= hi) ? 4u : 0u) | ((jd >= lo && jd <= hi) ? 8u : 0u);
+                    f &= fmask;
+                    if (f) {
+                        const int idx = wrow + r * 32 + lane;
+                        const int jg = cur_st * kSub + j;
+                        if (nev[r] < kCap) ev[(ci.row0 + idx) * kCap + nev[r]] = (uint32_t)jg | (f << 28);
+                        ++nev[r];
+                    }
+                }
+            }
+        }
+        ++nsub;
+        __syncwarp();
+        const int st = wk.next(fb, prune ? bound : INFINITY, false, refs_need);
+        if (st >= 0) {
+            if (lane == issued % NSLOT) slot_st = st;
+            if (lane == 0) ring_issue(ring, issued % NSLOT, cp + (int64_t)st * kSub * DP);
+            ++issued;
+        }
+    }
+    if (lane == 0) atomicAdd(work, (unsigned long long)nsub);
+#pragma unroll
+    for (int r = 0; r < kRT; ++r) {
+        const int idx = wrow + r * 32 + lane;
+        if (idx >= ci.n) continue;
+        const uint32_t self = band[r].lo > 0.0f ? 1u : 0u;  // the self pair counted as inside
+        const int64_t row = ci.row0 + idx;
+        cnt_out[row] = (int32_t)(cA[r] - self);
+        cnt_out[ws_rows + row] = (int32_t)(c2[r] - self);
+        cnt_out[2 * ws_rows + row] = (int32_t)(c3[r] - self);
+        ev_n[row] = nev[r];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // pass 2: certain counts in the three TE marginals + band events
 //   marginal 0 = y-past (A), 1 = y + y-past (m2), 2 = y-past + x-past (m3)
 //   A <= every marginal and the joint, so A > hi settles a pair (outside
@@ -1616,9 +1769,14 @@ static RescanFn rescan_table(int dy, int dx, int k) {
     return nullptr;
 }
 
-static CountFn count_table(int dy, int dx) {
+// Chunks of a few sub-tiles: nearly every reference needs every sub-tile,
+// so compaction only adds its overhead; the direct two-per-lane sweep wins.
+constexpr int kCompactMinRows = 4096;
+
+static CountFn count_table(int dy, int dx, int max_npad) {
 #define ENTE_CASE(a, b) \
-    if (dy == a && dx == b) return count_pass_kernel<a, b>;
+    if (dy == a && dx == b) \
+        return max_npad >= kCompactMinRows ? count_pass_kernel<a, b> : count_pass_direct_kernel<a, b>;
     ENTE_TE_LAYOUTS(ENTE_CASE)
 #undef ENTE_CASE
     return nullptr;
@@ -1651,7 +1809,7 @@ static bool match_te_layout(int dim, const uint32_t *masks, int n_marg, int &dy_
             else if (masks[m] == all_but_0) lay.slot[m] = 2;
             else ok = false;
         }
-        if (ok && count_table(dy, dim - 1 - dy) != nullptr) {
+        if (ok && count_table(dy, dim - 1 - dy, 0) != nullptr) {
             dy_out = dy;
             lay.dy = dy;
             lay.nout = n_marg;
@@ -1996,7 +2154,7 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
         uint32_t fmask = 8u;
         for (int o = 0; o < p.lay.nout; ++o) fmask |= 1u << p.lay.slot[o];
         ENTE_LAUNCH("count_pass", st,
-                    count_table(p.dy, p.dx)<<<nt, 32, 0, st>>>(w.pts32, w.fbox, w.info, w.tile0, n_chunks,
+                    count_table(p.dy, p.dx, p.max_npad)<<<nt, 32, 0, st>>>(w.pts32, w.fbox, w.info, w.tile0, n_chunks,
                                                                w.t32, ws_rows, prune, w.cnt3, w.ev,
                                                                w.ev_n, fmask, work + 1));
         ENTE_CUDA(cudaGetLastError());
