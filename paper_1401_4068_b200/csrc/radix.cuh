@@ -16,24 +16,27 @@
 
 namespace ente {
 
-constexpr int kSortThreads = 512;
-constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortThreads = 512;      // CTA size for large segments
+constexpr int kSortThreadsSmall = 128;  // ... for segments of <= kSortSmallN keys
+constexpr int kSortSmallN = 2048;
 constexpr int kSortItems = 8;  // keys per thread per tile
-constexpr int kSortTile = kSortThreads * kSortItems;
 
-struct SortSmem {
-    int wcnt[kSortWarps][256];  // per-warp digit counts, then their exclusive scan
-    int off[256];               // running output offset of each digit
+template <int T>
+struct SortSmemT {
+    int wcnt[T / 32][256];  // per-warp digit counts, then their exclusive scan
+    int off[256];           // running output offset of each digit
     int tile_total[256];
     int single;
 };
+using SortSmem = SortSmemT<kSortThreads>;
 
 // Sorts (keys, vals) of length n by the low `bits` bits of the keys.  The
 // result ends in (ka, va) when the function returns 0, in (kb, vb) when it
 // returns 1.  vals may be null (keys only).  Passes whose digit is shared by
 // every key are skipped.  Must be called by all kSortThreads threads.
-template <typename K, typename V>
-__device__ int cta_radix_sort(K *ka, K *kb, V *va, V *vb, int n, int bits, SortSmem &sm) {
+template <int T, typename K, typename V>
+__device__ int cta_radix_sort(K *ka, K *kb, V *va, V *vb, int n, int bits, SortSmemT<T> &sm) {
+    constexpr int kSortWarps = T / 32, kSortThreads = T, kSortTile = T * kSortItems;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
     int parity = 0;
@@ -47,10 +50,10 @@ __device__ int cta_radix_sort(K *ka, K *kb, V *va, V *vb, int n, int bits, SortS
         for (int i = tid; i < n; i += kSortThreads)
             atomicAdd(&sm.wcnt[warp][(int)((src[i] >> shift) & 255)], 1);
         __syncthreads();
-        if (tid < 256) {
+        for (int d = tid; d < 256; d += kSortThreads) {
             int t = 0;
-            for (int w = 0; w < kSortWarps; ++w) t += sm.wcnt[w][tid];
-            sm.tile_total[tid] = t;
+            for (int w = 0; w < kSortWarps; ++w) t += sm.wcnt[w][d];
+            sm.tile_total[d] = t;
             if (t == n) sm.single = 1;
         }
         __syncthreads();
@@ -102,15 +105,15 @@ __device__ int cta_radix_sort(K *ka, K *kb, V *va, V *vb, int n, int bits, SortS
                 __syncwarp();
             }
             __syncthreads();
-            if (tid < 256) {  // scan the warps' counts of digit tid
+            for (int d = tid; d < 256; d += kSortThreads) {  // scan the warps' counts of digit d
                 int run = 0;
 #pragma unroll
                 for (int w = 0; w < kSortWarps; ++w) {
-                    const int c = sm.wcnt[w][tid];
-                    sm.wcnt[w][tid] = run;
+                    const int c = sm.wcnt[w][d];
+                    sm.wcnt[w][d] = run;
                     run += c;
                 }
-                sm.tile_total[tid] = run;
+                sm.tile_total[d] = run;
             }
             __syncthreads();
 #pragma unroll
@@ -123,7 +126,7 @@ __device__ int cta_radix_sort(K *ka, K *kb, V *va, V *vb, int n, int bits, SortS
                 }
             }
             __syncthreads();
-            if (tid < 256) sm.off[tid] += sm.tile_total[tid];
+            for (int d = tid; d < 256; d += kSortThreads) sm.off[d] += sm.tile_total[d];
             // (the next tile's zeroing barrier orders this update)
         }
         K *t = src;

@@ -274,12 +274,13 @@ struct FilterCols {
     int f0, nf, bits;  // columns and Morton bits per column
 };
 
-__global__ void __launch_bounds__(kSortThreads) sort_kernel(
+template <int T>
+__global__ void __launch_bounds__(T) sort_kernel(
     const double *__restrict__ pts64, int dim, const ChunkInfo *__restrict__ info,
     const ColStats *__restrict__ stats, FilterCols fc, uint32_t *__restrict__ ka,
     uint32_t *__restrict__ kb, int32_t *__restrict__ va, int32_t *__restrict__ vb,
     int32_t *__restrict__ perm) {
-    __shared__ SortSmem sm;
+    __shared__ SortSmemT<T> sm;
     __shared__ double qlo[kMaxDim], qscale[kMaxDim];
     const ChunkInfo ci = info[blockIdx.x];
     if (!ci.ok32) return;
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_kernel(
     const double *p = pts64 + ci.row0 * dim;
     uint32_t *k0 = ka + ci.row0, *k1 = kb + ci.row0;
     int32_t *v0 = va + ci.row0, *v1 = vb + ci.row0;
-    for (int i = threadIdx.x; i < ci.n; i += kSortThreads) {
+    for (int i = threadIdx.x; i < ci.n; i += T) {
         uint32_t key = 0;
         uint32_t q[kMaxDim];
         for (int f = 0; f < fc.nf; ++f) {
@@ -308,9 +309,9 @@ __global__ void __launch_bounds__(kSortThreads) sort_kernel(
         v0[i] = i;
     }
     __syncthreads();
-    const int par = cta_radix_sort<uint32_t, int32_t>(k0, k1, v0, v1, ci.n, fc.nf * fc.bits, sm);
+    const int par = cta_radix_sort<T, uint32_t, int32_t>(k0, k1, v0, v1, ci.n, fc.nf * fc.bits, sm);
     const int32_t *res = par ? v1 : v0;
-    for (int i = threadIdx.x; i < ci.n; i += kSortThreads) perm[ci.row0 + i] = res[i];
+    for (int i = threadIdx.x; i < ci.n; i += T) perm[ci.row0 + i] = res[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -328,18 +329,19 @@ __device__ __forceinline__ uint32_t spread15(uint32_t v) {  // bits 0..14 -> eve
     return v;
 }
 
-__global__ void __launch_bounds__(kSortThreads) sort_pca_kernel(
+template <int T>
+__global__ void __launch_bounds__(T) sort_pca_kernel(
     const double *__restrict__ pts64, int dim, const ChunkInfo *__restrict__ info,
     const ColStats *__restrict__ stats, uint32_t *__restrict__ ka, uint32_t *__restrict__ kb,
     int32_t *__restrict__ va, int32_t *__restrict__ vb, const int32_t *__restrict__ cperm,
     int32_t *__restrict__ perm) {
-    __shared__ SortSmem sm;
-    __shared__ float red[4][kSortWarps];
+    __shared__ SortSmemT<T> sm;
+    __shared__ float red[4][(T / 32)];
     const ChunkInfo ci = info[blockIdx.x];
     if (!ci.ok32) return;
     const ColStats *cs = stats + blockIdx.x;
     if (!cs->use_pca) {  // keep the count pass's y-past Morton order
-        for (int i = threadIdx.x; i < ci.n; i += kSortThreads) perm[ci.row0 + i] = cperm[ci.row0 + i];
+        for (int i = threadIdx.x; i < ci.n; i += T) perm[ci.row0 + i] = cperm[ci.row0 + i];
         return;
     }
     const int P = dim < kPcaCols ? dim : kPcaCols;
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_pca_kernel(
             z1 += cs->axis[1][c] * x;
         }
     };
-    for (int i = threadIdx.x; i < ci.n; i += kSortThreads) {
+    for (int i = threadIdx.x; i < ci.n; i += T) {
         float z0, z1;
         proj(i, z0, z1);
         mn0 = fminf(mn0, z0);
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_pca_kernel(
         red[3][wid] = mx1;
     }
     __syncthreads();
-    for (int w = 0; w < kSortWarps; ++w) {
+    for (int w = 0; w < (T / 32); ++w) {
         mn0 = fminf(mn0, red[0][w]);
         mx0 = fmaxf(mx0, red[1][w]);
         mn1 = fminf(mn1, red[2][w]);
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_pca_kernel(
     const float q = 32767.0f;
     const float s0 = mx0 > mn0 ? q / (mx0 - mn0) : 0.0f;
     const float s1 = mx1 > mn1 ? q / (mx1 - mn1) : 0.0f;
-    for (int i = threadIdx.x; i < ci.n; i += kSortThreads) {
+    for (int i = threadIdx.x; i < ci.n; i += T) {
         float z0, z1;
         proj(i, z0, z1);
         const uint32_t a = (uint32_t)fminf(fmaxf((z0 - mn0) * s0, 0.0f), q);
@@ -396,9 +398,9 @@ __global__ void __launch_bounds__(kSortThreads) sort_pca_kernel(
         v0[i] = i;
     }
     __syncthreads();
-    const int par = cta_radix_sort<uint32_t, int32_t>(k0, k1, v0, v1, ci.n, 30, sm);
+    const int par = cta_radix_sort<T, uint32_t, int32_t>(k0, k1, v0, v1, ci.n, 30, sm);
     const int32_t *res = par ? v1 : v0;
-    for (int i = threadIdx.x; i < ci.n; i += kSortThreads) perm[ci.row0 + i] = res[i];
+    for (int i = threadIdx.x; i < ci.n; i += T) perm[ci.row0 + i] = res[i];
 }
 
 // kNN copy: fp32 rows in the kNN order + boxes over columns 0 .. 4*kKnnQ-1
@@ -2006,11 +2008,13 @@ static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Pl
         FilterCols sfc = p.fc;
         if (!prune) sfc.nf = 0;  // identity order
         ENTE_LAUNCH("sort", st,
-                    sort_kernel<<<n_chunks, kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats, sfc,
+                    (p.max_npad <= kSortSmallN ? sort_kernel<kSortThreadsSmall> : sort_kernel<kSortThreads>)
+                    <<<n_chunks, p.max_npad <= kSortSmallN ? kSortThreadsSmall : kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats, sfc,
                                                                    w.ka, w.kb, w.va, w.vb, w.perm));
         ENTE_CUDA(cudaGetLastError());
         ENTE_LAUNCH("sort_pca", st,
-                    sort_pca_kernel<<<n_chunks, kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats,
+                    (p.max_npad <= kSortSmallN ? sort_pca_kernel<kSortThreadsSmall> : sort_pca_kernel<kSortThreads>)
+                    <<<n_chunks, p.max_npad <= kSortSmallN ? kSortThreadsSmall : kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats,
                                                                        w.ka, w.kb, w.va, w.vb,
                                                                        w.perm, w.permk));
         ENTE_CUDA(cudaGetLastError());

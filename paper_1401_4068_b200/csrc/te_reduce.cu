@@ -135,11 +135,12 @@ struct RedChunk {
     int32_t pad_;
 };
 
-__global__ void __launch_bounds__(kSortThreads) te_reduce_kernel(
+template <int T>
+__global__ void __launch_bounds__(T) te_reduce_kernel(
     const int32_t *__restrict__ counts, int64_t total_rows, const RedChunk *__restrict__ chunks,
     const double *__restrict__ psi, int64_t table_len, double psi_k, uint64_t *__restrict__ ka,
     uint64_t *__restrict__ kb, double *__restrict__ out_te) {
-    __shared__ SortSmem sm;
+    __shared__ SortSmemT<T> sm;
     __shared__ int bad;
     __shared__ int n_leaves;
     const RedChunk ch = chunks[blockIdx.x];
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(kSortThreads) te_reduce_kernel(
     uint64_t *dst = kb + ch.row0;
     if (threadIdx.x == 0) bad = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += kSortThreads) {
+    for (int i = threadIdx.x; i < n; i += T) {
         const int64_t row = ch.row0 + i;
         const int a = counts[row], b = counts[total_rows + row], c = counts[2 * total_rows + row];
         double v = 0.0;
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(kSortThreads) te_reduce_kernel(
         if (threadIdx.x == 0) out_te[blockIdx.x] = __longlong_as_double(0x7FF8000000000000ll);
         return;
     }
-    const int parity = cta_radix_sort<uint64_t, int>(src, dst, nullptr, nullptr, n, 64, sm);
+    const int parity = cta_radix_sort<T, uint64_t, int>(src, dst, nullptr, nullptr, n, 64, sm);
     const double sum = pairwise_cta(parity ? dst : src, n, parity ? src : dst, &n_leaves);
     if (threadIdx.x == 0) out_te[blockIdx.x] = __dadd_rn(psi_k, __ddiv_rn(sum, (double)n));
 }
@@ -190,6 +191,7 @@ extern "C" int ente_te_reduce(const int32_t *counts, int64_t total_rows, const e
         return ENTE_ERR_ARG;
     }
     int64_t rows = 0;
+    int max_n = 0;
     std::vector<RedChunk> h(n_chunks);
     for (int c = 0; c < n_chunks; ++c) {
         if (chunks[c].n < 1 || chunks[c].row0 < 0 || chunks[c].row0 + chunks[c].n > total_rows) {
@@ -198,6 +200,7 @@ extern "C" int ente_te_reduce(const int32_t *counts, int64_t total_rows, const e
         }
         h[c].row0 = chunks[c].row0;
         h[c].n = chunks[c].n;
+        max_n = max_n > chunks[c].n ? max_n : chunks[c].n;
         rows = rows > chunks[c].row0 + chunks[c].n ? rows : chunks[c].row0 + chunks[c].n;
     }
     Arena a(workspace, ws_bytes);
@@ -211,7 +214,8 @@ extern "C" int ente_te_reduce(const int32_t *counts, int64_t total_rows, const e
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ENTE_CUDA(cudaMemcpyAsync(dch, h.data(), sizeof(RedChunk) * n_chunks, cudaMemcpyHostToDevice, st));
     ENTE_LAUNCH("te_reduce", st,
-                te_reduce_kernel<<<n_chunks, kSortThreads, 0, st>>>(counts, total_rows, dch,
+                (max_n <= kSortSmallN ? te_reduce_kernel<kSortThreadsSmall> : te_reduce_kernel<kSortThreads>)
+                <<<n_chunks, max_n <= kSortSmallN ? kSortThreadsSmall : kSortThreads, 0, st>>>(counts, total_rows, dch,
                                                                   psi_table, table_len, psi_k, ka,
                                                                   kb, out_te));
     ENTE_CUDA(cudaGetLastError());
