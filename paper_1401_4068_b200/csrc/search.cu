@@ -46,11 +46,17 @@ constexpr int kSub = 32;                    // candidate rows per sub-tile (one 
 constexpr int kWarpRefs = 32 * kRT;         // references per sweep CTA (one warp)
 constexpr int kGate = 4;                    // gate columns in the Morton key and the boxes
 // minimum resident sweep CTAs (one warp each) per SM: caps the registers
+#ifndef ENTE_KNN_NSLOT
+#define ENTE_KNN_NSLOT 4
+#endif
+#ifndef ENTE_CNT_NSLOT
+#define ENTE_CNT_NSLOT 2
+#endif
 #ifndef ENTE_CNT_MINB
-#define ENTE_CNT_MINB 21
+#define ENTE_CNT_MINB 32
 #endif
 #ifndef ENTE_KNN_MINB
-#define ENTE_KNN_MINB 21
+#define ENTE_KNN_MINB 32
 #endif
 constexpr int kKnnQ = 2;                    // kNN sub-tile boxes: 4 * kKnnQ columns from 0
 
@@ -783,7 +789,8 @@ __global__ void __launch_bounds__(32, ENTE_KNN_MINB) knn_pass_kernel(
     const int32_t *__restrict__ kmap, float *__restrict__ t32_out, int32_t *__restrict__ L_out,
     unsigned long long *__restrict__ work) {
     using L = Lay<DY, DX>;
-    constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG, NSLOT = L::NSLOT;
+    constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG;
+    constexpr int NSLOT = L::NSLOT < ENTE_KNN_NSLOT ? L::NSLOT : ENTE_KNN_NSLOT;
     constexpr int NBC = D < 4 * kKnnQ ? D : 4 * kKnnQ;  // box columns 0 .. NBC-1
     __shared__ __align__(128) Ring<DP, NSLOT> ring;
     const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
@@ -1082,8 +1089,8 @@ __global__ void __launch_bounds__(32, ENTE_CNT_MINB) count_pass_kernel(
     uint32_t *__restrict__ ev, int32_t *__restrict__ ev_n, uint32_t fmask,
     unsigned long long *__restrict__ work) {
     using L = Lay<DY, DX>;
-    constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG, NSLOT = L::NSLOT;
-    constexpr int NR = 32 * kRT;
+    constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG;
+    constexpr int NSLOT = L::NSLOT < ENTE_CNT_NSLOT ? L::NSLOT : ENTE_CNT_NSLOT;
     __shared__ __align__(128) Ring<DP, NSLOT> ring;
     __shared__ __align__(16) CountRefs<DP, NSLOT> rs;
     const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
@@ -1183,23 +1190,13 @@ __global__ void __launch_bounds__(32, ENTE_CNT_MINB) count_pass_kernel(
             uint32_t cA = 0u, c2 = 0u, c3 = 0u;
             int nev = active ? rs.nev[ri] : 0;
             const int64_t evrow = (ci.row0 + wrow + ri) * kCap;
-            float4 nxt[NQ];
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) nxt[q] = tile[q];
-#pragma unroll 2
-            for (int j = 0; j < kSub; ++j) {
-                float4 cur[NQ];
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) cur[q] = nxt[q];
-                if (j + 1 < kSub) {
-#pragma unroll
-                    for (int q = 0; q < NQ; ++q) nxt[q] = tile[(j + 1) * NQ + q];
-                }
+            // one candidate row against this lane's reference
+            auto visit = [&](const float4 (&cur)[NQ], int j) {
                 const float2 *c = reinterpret_cast<const float2 *>(cur);
                 float a[2 * NP];
                 diff_pairs<D, 0, PG>(ref, c, a);
                 const float A = maxabs0<1, 1 + DY, 2 * NP>(a);
-                if (!__any_sync(0xffffffffu, A <= hi)) continue;
+                if (!__any_sync(0xffffffffu, A <= hi)) return;
                 diff_pairs<D, PG, NP>(ref, c, a);
                 const float m2 = fmaxf(A, fabsf(a[0]));
                 const float m3 = maxabs<1 + DY, D, 2 * NP>(a, A);
@@ -1221,6 +1218,20 @@ __global__ void __launch_bounds__(32, ENTE_CNT_MINB) count_pass_kernel(
                         ++nev;
                     }
                 }
+            };
+            // ping-pong row registers: the next row's LDS overlaps this row's math
+            float4 ra[NQ], rb[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) ra[q] = tile[q];
+            for (int j = 0; j < kSub; j += 2) {
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) rb[q] = tile[(j + 1) * NQ + q];
+                visit(ra, j);
+                if (j + 2 < kSub) {
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) ra[q] = tile[(j + 2) * NQ + q];
+                }
+                visit(rb, j + 1);
             }
             if (active) {
                 rs.cnt[0][ri] += cA;
