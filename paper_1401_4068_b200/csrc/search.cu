@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(T) sort_kernel(
 
 // ---------------------------------------------------------------------------
 // kNN order: Morton order of the projections on the chunk's two leading
-// principal axes (15 bits each).  Embedded dynamics concentrate near a
+// principal axes (12 bits each).  Embedded dynamics concentrate near a
 // low-dimensional manifold; a 2-D order along it keeps 32-row sub-tiles
 // compact in every column, which the kNN pass's all-column boxes exploit.
 // ---------------------------------------------------------------------------
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(T) sort_pca_kernel(
         mn1 = fminf(mn1, red[2][w]);
         mx1 = fmaxf(mx1, red[3][w]);
     }
-    const float q = 32767.0f;
+    const float q = 4095.0f;  // 12 bits per axis: 24-bit keys, three radix passes
     const float s0 = mx0 > mn0 ? q / (mx0 - mn0) : 0.0f;
     const float s1 = mx1 > mn1 ? q / (mx1 - mn1) : 0.0f;
     for (int i = threadIdx.x; i < ci.n; i += T) {
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(T) sort_pca_kernel(
         v0[i] = i;
     }
     __syncthreads();
-    const int par = cta_radix_sort<T, uint32_t, int32_t>(k0, k1, v0, v1, ci.n, 30, sm);
+    const int par = cta_radix_sort<T, uint32_t, int32_t>(k0, k1, v0, v1, ci.n, 24, sm);
     const int32_t *res = par ? v1 : v0;
     for (int i = threadIdx.x; i < ci.n; i += T) perm[ci.row0 + i] = res[i];
 }
@@ -1839,7 +1839,7 @@ static FilterCols filter_cols(int dy) {
     FilterCols fc{};
     fc.f0 = 1;
     fc.nf = std::min(dy, kGate);
-    fc.bits = fc.nf > 0 ? std::min(10, 30 / fc.nf) : 0;
+    fc.bits = fc.nf > 0 ? std::min(16, 24 / fc.nf) : 0;  // 24-bit keys: three radix passes
     return fc;
 }
 
