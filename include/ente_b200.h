@@ -106,6 +106,24 @@ int ente_knn_indices(const double *pts64, int64_t total_rows, int dim, const ent
                      void *workspace, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * ente_ragwitz_errors -- squared errors of the cross-repetition local
+ * predictor for (dim, delay) candidate embeddings (Ragwitz criterion).
+ *
+ * Replaces: ente.embedding._local_predictor_sq_errors  embedding.py:123-165
+ *           (caller: optimize_embedding embedding.py:168-210)
+ *
+ *   values       [dev]  [reps x n_samp] fp64 ensemble, repetition-major
+ *   anchors_r/t  [dev]  [n_anchor] int32 repetition and 0-based index of the
+ *                       anchor's most recent embedded sample
+ *   k_pred              neighbours averaged, 1..16
+ *   out_err      [dev]  [n_anchor] fp64 (prediction - next sample)^2,
+ *                       bit-identical to the reference
+ * ------------------------------------------------------------------------- */
+int ente_ragwitz_errors(const double *values, int reps, int n_samp, int d, int tau,
+                        const int32_t *anchors_r, const int32_t *anchors_t, int n_anchor,
+                        int k_pred, double *out_err, void *stream);
+
+/* ---------------------------------------------------------------------------
  * ente_radius_counts -- strict counts #{j != i : maxnorm_marg(p_i, p_j) < r_i}
  * for caller-given radii (fp64, exact), one count array per marginal.
  *

@@ -212,3 +212,28 @@ def analyze_pair(xv, yv, spec_x, spec_y, u_candidates, window, k=4, n_surrogates
     p = (cnt + 1) / (n_surrogates + 1) if conservative else cnt / n_surrogates
     return {"u_selected": u_best, "te_value": te_best, "te_curve": curve,
             "surrogate_values": surr, "p_value": p}
+
+
+def ragwitz_errors(values, d, tau, anchors_r, anchors_t, k_pred):
+    """embedding.py:123-165 restated: k_pred nearest cross-repetition embedded points in
+    lexicographic (max-norm distance, scan position r2 asc / t2 asc) order; the
+    prediction sums their next samples in that order, / k_pred; squared error."""
+    v = np.asarray(values, dtype=np.float64)
+    n_rep, n_samp = v.shape
+    span_lo = (d - 1) * tau
+    t2 = np.arange(span_lo, n_samp - 1)
+    errs = np.empty(len(anchors_r))
+    for a, (r0, t0) in enumerate(zip(anchors_r, anchors_t)):
+        ref = v[r0, t0 - tau * np.arange(d)]
+        others = [r for r in range(n_rep) if r != r0]
+        emb = np.stack([v[others][:, t2 - c * tau] for c in range(d)], axis=-1)  # [R-1, T, d]
+        dist = np.abs(emb - ref).max(axis=-1).ravel()
+        nxt = v[others][:, t2 + 1].ravel()
+        order = np.argsort(dist, kind="stable")[:k_pred]  # stable = scan order on ties
+        pred = 0.0
+        for q in order:
+            pred += nxt[q]
+        pred /= k_pred
+        diff = pred - v[r0, t0 + 1]
+        errs[a] = diff * diff
+    return errs

@@ -45,6 +45,7 @@ def _declare(L):
         "ente_last_error": ([], ctypes.c_char_p),
         "ente_search_workspace_size": ([cp, i32, i32, i32, i32], sz),
         "ente_search": ([vp, i64, i32, cp, i32, u32p, i32, i32, vp, vp, vp, vp, sz, vp], i32),
+        "ente_ragwitz_errors": ([vp, i32, i32, i32, i32, vp, vp, i32, i32, vp, vp], i32),
         "ente_knn_indices": ([vp, i64, i32, cp, i32, i32, vp, vp, vp, vp, sz, vp], i32),
         "ente_radius_counts_workspace_size": ([i32], sz),
         "ente_radius_counts": ([vp, i64, i32, cp, i32, u32p, i32, vp, vp, vp, vp, sz, vp], i32),

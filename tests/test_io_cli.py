@@ -66,8 +66,8 @@ def test_cli_exit_codes(tmp_path, capsys):
                      "--samples", "60", "--out", prefix]) == 0
     assert cli.main(["validate", prefix + "_X.bin"]) == 0
     assert cli.main(["analyze", "--source", prefix + "_X.bin", "--target", prefix + "_Y.bin",
-                     "--window", "30:40", "--u", "1:2", "--ragwitz", "--out",
-                     str(tmp_path / "o.json")]) == 1
+                     "--window", "30:40", "--u", "1:2", "--ragwitz", "--ragwitz-dims", "x",
+                     "--out", str(tmp_path / "o.json")]) == 1
     assert cli.main(["analyze", "--source", prefix + "_X.bin", "--target", prefix + "_Y.bin",
                      "--window", "40:30", "--u", "1", "--out", str(tmp_path / "o.json")]) == 1
 
