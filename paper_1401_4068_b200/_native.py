@@ -118,18 +118,23 @@ def ptr(t: torch.Tensor) -> int:
 
 
 class _Workspace(threading.local):
-    buf = None
+    bufs = None
 
 
 _ws = _Workspace()
 
 
-def workspace(nbytes: int) -> torch.Tensor:
-    """A per-thread device scratch buffer of at least nbytes (grown on demand)."""
-    buf = _ws.buf
+def workspace(nbytes: int, tag: str = "") -> torch.Tensor:
+    """A per-thread (and per-tag: one per concurrent stream) device scratch buffer of
+    at least nbytes, grown on demand."""
+    if _ws.bufs is None:
+        _ws.bufs = {}
+    buf = _ws.bufs.get(tag)
     if buf is None or buf.numel() < nbytes or buf.device != device():
+        _ws.bufs[tag] = None
+        del buf
         buf = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=device())
-        _ws.buf = buf
+        _ws.bufs[tag] = buf
     return buf
 
 

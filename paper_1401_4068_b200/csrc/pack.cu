@@ -10,6 +10,7 @@
 // shuffling the target's repetitions permutes only the y columns.
 #include <cuda_runtime.h>
 
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -51,28 +52,27 @@ __global__ void __launch_bounds__(256) pack_te_kernel(
 
 using namespace ente;
 
-// Per-device grow-only item table.  Stream-ordered use on one stream per
-// device (the library's contract): a later copy into the table is ordered
-// after the earlier kernel that read it.
-static PackItem *item_table(int n) {
+// Per-(device, stream) grow-only item table.  Calls on one stream are
+// ordered, so a later copy into the table lands after the earlier kernel
+// that read it; concurrent streams get separate tables.
+static PackItem *item_table(int n, cudaStream_t st) {
     static std::mutex mu;
-    static PackItem *tab[64] = {nullptr};
-    static int cap[64] = {0};
+    static std::map<std::pair<int, cudaStream_t>, std::pair<PackItem *, int>> tabs;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64) return nullptr;
     std::lock_guard<std::mutex> lk(mu);
-    if (cap[dev] < n) {
-        if (tab[dev]) cudaFree(tab[dev]);  // synchronises: rare (growth only)
-        tab[dev] = nullptr;
-        cap[dev] = 0;
+    auto &t = tabs[{dev, st}];
+    if (t.second < n) {
+        if (t.first) cudaFree(t.first);  // synchronises: rare (growth only)
+        t.first = nullptr;
+        t.second = 0;
         const int want = n < 4096 ? 4096 : n + n / 2;
         void *p = nullptr;
         if (cudaMalloc(&p, sizeof(PackItem) * (size_t)want) != cudaSuccess) return nullptr;
-        tab[dev] = static_cast<PackItem *>(p);
-        cap[dev] = want;
+        t.first = static_cast<PackItem *>(p);
+        t.second = want;
     }
-    return tab[dev];
+    return t.first;
 }
 
 extern "C" int ente_pack_te_items(const double *x, const double *y, int reps, int n_samples,
@@ -106,7 +106,7 @@ extern "C" int ente_pack_te_items(const double *x, const double *y, int reps, in
     // stream-ordered copy (no per-call allocation: stream-ordered
     // allocations are trimmed at every synchronisation, which cost
     // 10-600 ms per call)
-    PackItem *ditems = item_table(n_items);
+    PackItem *ditems = item_table(n_items, st);
     if (!ditems) {
         set_error("ente_pack_te: cannot allocate the item table (%d items)", n_items);
         return ENTE_ERR_CUDA;

@@ -80,7 +80,8 @@ def column_mask(cols, dim: int) -> int:
 # ---------------------------------------------------------------------------
 # device-level entry points (tensors in, tensors out; used by ksg / bench)
 # ---------------------------------------------------------------------------
-def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int, reuse: bool = False):
+def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int, reuse: bool = False,
+                  tag: str = ""):
     """ente_search on a device-resident [rows, dim] fp64 matrix.
 
     Returns (eps [rows] f64, counts [n_marg, rows] int32, status [n_chunks] int32),
@@ -94,15 +95,15 @@ def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int, reuse: bool = F
     table = nat.chunk_table(rows0, ns)
     marr = nat.masks_array(masks)
     if reuse:
-        eps = nat.scratch("search.eps", (rows,), torch.float64)
-        counts = nat.scratch("search.counts", (max(1, len(masks)), rows), torch.int32)
-        status = nat.scratch("search.status", (max(1, len(ns)),), torch.int32)
+        eps = nat.scratch("search.eps" + tag, (rows,), torch.float64)
+        counts = nat.scratch("search.counts" + tag, (max(1, len(masks)), rows), torch.int32)
+        status = nat.scratch("search.status" + tag, (max(1, len(ns)),), torch.int32)
     else:
         eps = torch.empty(rows, dtype=torch.float64, device=pts64.device)
         counts = torch.empty((max(1, len(masks)), rows), dtype=torch.int32, device=pts64.device)
         status = torch.empty(max(1, len(ns)), dtype=torch.int32, device=pts64.device)
     need = L.ente_search_workspace_size(table, len(ns), dim, len(masks), int(k))
-    ws = nat.workspace(need)
+    ws = nat.workspace(need, tag)
     nat.check(L.ente_search(nat.ptr(pts64), rows, dim, table, len(ns), marr, len(masks), int(k),
                             nat.ptr(eps), nat.ptr(counts), nat.ptr(status), nat.ptr(ws), ws.numel(),
                             nat.stream_handle()), "ente_search")

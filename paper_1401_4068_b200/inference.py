@@ -16,6 +16,7 @@ reference derives them (numpy SeedSequence / Generator) and cached per
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -27,8 +28,11 @@ from .embedding import EmbeddingSpec, PointSetBundle, check_assembly
 from .exceptions import EnteError, InvalidPermutation, KTooLarge, UnknownMethod
 from .ksg import _raise_status, te_chunks_device
 
-# rows per device wave (fp64 joint + fp32 copy + counts + events ~ 150 B/row)
+# rows per device wave (fp64 joint + fp32 copies + counts + events ~ 240 B/row)
 MAX_ROWS_PER_WAVE = 1 << 28
+# a wave runs as up to SUB_BATCHES sub-batches on two streams (>= MIN_SUB_BATCH chunks each)
+SUB_BATCHES = int(os.environ.get("ENTE_SUB_BATCHES", "1"))
+MIN_SUB_BATCH = 64
 
 
 @dataclass(frozen=True)
@@ -203,9 +207,35 @@ class PairPipeline:
         return np.ascontiguousarray(uniq[inv.reshape(-1)])
 
     def _wave(self, it: np.ndarray) -> np.ndarray:
+        """One device batch, split into sub-batches alternating over two CUDA
+        streams so that one sub-batch's latency-bound kernels (pack, jitter,
+        sorts, gathers, reduction) overlap another's compute-bound sweeps.
+        Statuses are read once at the end."""
+        n = len(it)
+        nsub = 1 if n < 2 * MIN_SUB_BATCH else min(SUB_BATCHES, n // MIN_SUB_BATCH)
+        bounds = np.linspace(0, n, nsub + 1).astype(int)
+        states = self._states(it)
+        main = torch.cuda.current_stream()
+        streams = _streams(min(2, nsub))
+        outs = []
+        for b in range(nsub):
+            lo, hi = int(bounds[b]), int(bounds[b + 1])
+            stream = streams[b % len(streams)]
+            stream.wait_stream(main)
+            with torch.cuda.stream(stream):
+                outs.append(self._sub(it[lo:hi], states[lo:hi], f".s{b % len(streams)}"))
+        for stream in streams:
+            main.wait_stream(stream)
+        te = torch.cat([t for t, _ in outs]).cpu().numpy()
+        st = torch.cat([s for _, s in outs]).cpu().numpy()
+        if (st != 0).any():
+            _raise_status(int(st[np.flatnonzero(st)[0]]))
+        return te
+
+    def _sub(self, it: np.ndarray, states: np.ndarray, tag: str):
         L = nat.lib()
         n = len(it)
-        pts = nat.scratch("pipe.joint", (n * self.m, self.dim), torch.float64)
+        pts = nat.scratch("pipe.joint" + tag, (n * self.m, self.dim), torch.float64)
         perms_ptr = nat.ptr(self.perm_dev) if self.perm_dev is not None else None
         nat.check(L.ente_pack_te_items(nat.ptr(self.x), nat.ptr(self.y), self.reps,
                                        self.n_samples, self.sx.dim, self.sx.delay, self.sy.dim,
@@ -215,11 +245,22 @@ class PairPipeline:
                   "ente_pack_te_items")
         rows0 = np.arange(n, dtype=np.int64) * self.m
         ns = np.full(n, self.m, dtype=np.int64)
-        te, st = te_chunks_device(pts, rows0, ns, self.sy.dim, self.sx.dim, self.cfg.k,
-                                  self.cfg.jitter_amplitude, self._states(it))
-        if te is None:
-            _raise_status(int(st[np.flatnonzero(st)[0]]))
-        return te.cpu().numpy()
+        return te_chunks_device(pts, rows0, ns, self.sy.dim, self.sx.dim, self.cfg.k,
+                                self.cfg.jitter_amplitude, np.ascontiguousarray(states),
+                                sync=False, tag=tag)
+
+
+_STREAMS: dict = {}
+
+
+def _streams(count: int):
+    """Per-device side streams for sub-batch overlap (created once)."""
+    key = (torch.cuda.current_device(), count)
+    s = _STREAMS.get(key)
+    if s is None:
+        s = [torch.cuda.Stream() for _ in range(count)]
+        _STREAMS[key] = s
+    return s
 
 
 def analyze_pair(source: EnsembleSeries, target: EnsembleSeries,

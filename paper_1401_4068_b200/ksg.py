@@ -59,14 +59,14 @@ class _PsiTable:
 _PSI = _PsiTable()
 
 
-def te_reduce_device(counts: torch.Tensor, rows0, ns, k: int) -> torch.Tensor:
+def te_reduce_device(counts: torch.Tensor, rows0, ns, k: int, tag: str = "") -> torch.Tensor:
     """ente_te_reduce over a [3, rows] int32 device count matrix; returns [n_chunks] f64."""
     L = nat.lib()
     rows = counts.shape[1]
     psi = _PSI.get(int(np.max(ns)) + 2)
     out = torch.empty(len(ns), dtype=torch.float64, device=counts.device)
     table = nat.chunk_table(rows0, ns)
-    ws = nat.workspace(L.ente_te_reduce_workspace_size(table, len(ns)))
+    ws = nat.workspace(L.ente_te_reduce_workspace_size(table, len(ns)), tag)
     nat.check(L.ente_te_reduce(nat.ptr(counts), rows, table, len(ns), nat.ptr(psi), psi.numel(),
                                float(special.digamma(k)), nat.ptr(out), nat.ptr(ws), ws.numel(),
                                nat.stream_handle()), "ente_te_reduce")
@@ -86,7 +86,8 @@ def te_from_counts(counts: TermCounts) -> float:
     return float(te_reduce_device(mat, [0], [a.size], counts.k).cpu()[0])
 
 
-def jitter_device(pts64: torch.Tensor, rows0, ns, amplitude: float, seeds) -> torch.Tensor:
+def jitter_device(pts64: torch.Tensor, rows0, ns, amplitude: float, seeds,
+                  tag: str = "") -> torch.Tensor:
     """ente_jitter in place on a device [rows, dim] matrix; returns the status tensor."""
     L = nat.lib()
     dim = pts64.shape[1]
@@ -99,7 +100,7 @@ def jitter_device(pts64: torch.Tensor, rows0, ns, amplitude: float, seeds) -> to
             st = nat.pcg_states(seeds, [n * dim for n in ns])
         states = st.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_uint64))
     status = torch.zeros(len(ns), dtype=torch.int32, device=pts64.device)
-    ws = nat.workspace(L.ente_jitter_workspace_size(len(ns), dim))
+    ws = nat.workspace(L.ente_jitter_workspace_size(len(ns), dim), tag)
     nat.check(L.ente_jitter(nat.ptr(pts64), dim, table, len(ns), states, float(amplitude),
                             nat.ptr(status), nat.ptr(ws), ws.numel(), nat.stream_handle()),
               "ente_jitter")
@@ -115,19 +116,24 @@ def te_masks(d_y: int, d_x: int):
 
 
 def te_chunks_device(pts64: torch.Tensor, rows0, ns, d_y: int, d_x: int, k: int,
-                     amplitude: float, seeds):
+                     amplitude: float, seeds, sync: bool = True, tag: str = ""):
     """jitter -> checks -> search -> reduce for TE-layout chunks already on the device.
 
-    Returns (te [n_chunks] f64 device tensor, status numpy array).  The status
-    read-back is the only host synchronisation.
+    sync=True: returns (te [n_chunks] f64 device tensor or None, status numpy
+    array); the status read-back after the jitter checks is the only host
+    synchronisation, and chunks are not searched when any check failed.
+    sync=False: everything is queued on the current stream and (te, status)
+    come back as device tensors; the caller reads status before using te
+    (a failed chunk's TE is meaningless).  `tag` selects per-stream scratch.
     """
-    status = jitter_device(pts64, rows0, ns, amplitude, seeds)
-    st = status.cpu().numpy()
-    if (st != 0).any():
-        return None, st
-    _, counts, sstatus = search_device(pts64, rows0, ns, te_masks(d_y, d_x), k, reuse=True)
-    te = te_reduce_device(counts, rows0, ns, k)
-    return te, st
+    status = jitter_device(pts64, rows0, ns, amplitude, seeds, tag)
+    if sync:
+        st = status.cpu().numpy()
+        if (st != 0).any():
+            return None, st
+    _, counts, _ = search_device(pts64, rows0, ns, te_masks(d_y, d_x), k, reuse=True, tag=tag)
+    te = te_reduce_device(counts, rows0, ns, k, tag)
+    return (te, st) if sync else (te, status)
 
 
 def _raise_status(code: int):
