@@ -58,6 +58,12 @@ constexpr int kGate = 4;                    // gate columns in the Morton key an
 #ifndef ENTE_KNN_MINB
 #define ENTE_KNN_MINB 32
 #endif
+// resident one-warp sweep CTAs per SM by layout width: 32 (64 registers)
+// up to D = 7, fewer for wider layouts so their references stay in registers
+__host__ __device__ constexpr int sweep_minb(int D, int cap) {
+    return D <= 7 ? cap : (D <= 9 ? (cap < 28 ? cap : 28) : (D <= 11 ? (cap < 24 ? cap : 24)
+                                                              : (D <= 13 ? (cap < 20 ? cap : 20) : 16)));
+}
 constexpr int kKnnQ = 2;                    // kNN sub-tile boxes: 4 * kKnnQ columns from 0
 
 // per-chunk column statistics (fp64): mean, min, max of the raw values
@@ -783,7 +789,7 @@ __device__ __forceinline__ void ring_issue(Ring<DP, NSLOT> &ring, int slot, cons
 // lane l owns sorted rows wrow + r*32 + l, r < kRT
 // ---------------------------------------------------------------------------
 template <int DY, int DX, int S>
-__global__ void __launch_bounds__(32, ENTE_KNN_MINB) knn_pass_kernel(
+__global__ void __launch_bounds__(32, S > 8 ? 16 : sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) knn_pass_kernel(
     const float *__restrict__ pts32, const float *__restrict__ fbox,
     const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks, int k, int prune,
     const int32_t *__restrict__ kmap, float *__restrict__ t32_out, int32_t *__restrict__ L_out,
@@ -911,7 +917,7 @@ __global__ void __launch_bounds__(32, ENTE_KNN_MINB) knn_pass_kernel(
 //   everywhere, no event) after the gate columns alone
 // ---------------------------------------------------------------------------
 template <int DY, int DX>
-__global__ void __launch_bounds__(32, ENTE_CNT_MINB) count_pass_direct_kernel(
+__global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) count_pass_direct_kernel(
     const float *__restrict__ pts32, const float *__restrict__ fbox,
     const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks,
     const float *__restrict__ t32_in, int64_t ws_rows, int prune, int32_t *__restrict__ cnt_out,
@@ -1082,7 +1088,7 @@ struct CountRefs {
 };
 
 template <int DY, int DX>
-__global__ void __launch_bounds__(32, ENTE_CNT_MINB) count_pass_kernel(
+__global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) count_pass_kernel(
     const float *__restrict__ pts32, const float *__restrict__ fbox,
     const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks,
     const float *__restrict__ t32_in, int64_t ws_rows, int prune, int32_t *__restrict__ cnt_out,
