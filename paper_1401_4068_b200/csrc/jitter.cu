@@ -77,11 +77,11 @@ __global__ void __launch_bounds__(32) jitter_std_kernel(const double *__restrict
     if (col >= dim) return;
     const double *p = pts + c.row0 * dim + col;
     double s = 0.0;
-#pragma unroll 8
+#pragma unroll 32
     for (int r = 0; r < c.n; ++r) s = __dadd_rn(s, p[(int64_t)r * dim]);
     const double mean = __ddiv_rn(s, (double)c.n);
     double v = 0.0;
-#pragma unroll 8
+#pragma unroll 32
     for (int r = 0; r < c.n; ++r) {
         const double d = __dsub_rn(p[(int64_t)r * dim], mean);
         v = __dadd_rn(v, __dmul_rn(d, d));

@@ -66,6 +66,19 @@ __host__ __device__ constexpr int sweep_minb(int D, int cap) {
 }
 constexpr int kKnnQ = 2;                    // kNN sub-tile boxes: 4 * kKnnQ columns from 0
 
+// fp32 row writer of the gathers: columns are collected in a float4 register
+// and written as one 16-byte store per quad (rows are 16-B aligned, D padded
+// to a multiple of 4) instead of one 4-byte store per column
+#define STORE_COL(q4, col, v)                                   \
+    do {                                                        \
+        switch ((col) & 3) {                                    \
+            case 0: quad.x = (v); break;                        \
+            case 1: quad.y = (v); break;                        \
+            case 2: quad.z = (v); break;                        \
+            default: quad.w = (v); (q4)[(col) >> 2] = quad;     \
+        }                                                       \
+    } while (0)
+
 // per-chunk column statistics (fp64): mean, min, max of the raw values
 constexpr int kPcaCols = 8;  // principal axes over the first <= 8 columns
 
@@ -435,14 +448,15 @@ __global__ void __launch_bounds__(kTJ) gather_knn_kernel(
         const int32_t o = valid ? permk[ci.row0 + s] : 0;
         const int64_t orig = ci.row0 + o;
         if (valid) kmap[ci.row0 + s] = inv[orig];
-        float *q = pts32 + (ci.prow0 + s) * dp;
+        float4 *q4 = reinterpret_cast<float4 *>(pts32 + (ci.prow0 + s) * dp);
+        float4 quad = make_float4(0.f, 0.f, 0.f, 0.f);
         const int64_t sub = ci.prow0 / kSub + stage * (kTJ / kSub) + warp;
         for (int col = 0; col < dp; ++col) {
             float v = 0.0f;
             if (col < dim)
                 v = valid ? __double2float_rn(__dsub_rn(pts64[orig * dim + col], cs->mean[col]))
                           : INFINITY;
-            q[col] = v;
+            STORE_COL(q4, col, v);
             if (col < NB) {  // warp-uniform
                 float lo = 0.0f, hi = 0.0f;
                 if (col < dim) {
@@ -464,6 +478,7 @@ __global__ void __launch_bounds__(kTJ) gather_knn_kernel(
             for (int col = dp; col < NB; ++col) fbox[sub * 2 * NB + col] = fbox[sub * 2 * NB + NB + col] = 0.0f;
     }
 }
+
 
 // ---------------------------------------------------------------------------
 // gather: sorted fp32 rows (centred, D padded to DP) + per-32-row boxes over
@@ -487,14 +502,15 @@ __global__ void __launch_bounds__(kTJ) gather_kernel(const double *__restrict__ 
         const bool valid = s < ci.n;
         const int64_t orig = valid ? ci.row0 + perm[ci.row0 + s] : 0;
         if (valid && inv) inv[orig] = s;
-        float *q = pts32 + (ci.prow0 + s) * dp;
+        float4 *q4 = reinterpret_cast<float4 *>(pts32 + (ci.prow0 + s) * dp);
+        float4 quad = make_float4(0.f, 0.f, 0.f, 0.f);
         const int64_t sub = ci.prow0 / kSub + stage * (kTJ / kSub) + warp;
         for (int col = 0; col < dp; ++col) {
             float v = 0.0f;
             if (col < dim)
                 v = valid ? __double2float_rn(__dsub_rn(pts64[orig * dim + col], cs->mean[col]))
                           : INFINITY;
-            q[col] = v;
+            STORE_COL(q4, col, v);
             const int g = col - fc.f0;
             if (g >= 0 && g < kGate) {  // warp-uniform
                 float lo = 0.0f, hi = 0.0f;
