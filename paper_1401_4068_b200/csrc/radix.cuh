@@ -30,19 +30,20 @@ struct SortSmemT {
 };
 using SortSmem = SortSmemT<kSortThreads>;
 
-// Sorts (keys, vals) of length n by the low `bits` bits of the keys.  The
+// Sorts (keys, vals) of length n by key bits [shift0, shift0 + bits).  The
 // result ends in (ka, va) when the function returns 0, in (kb, vb) when it
 // returns 1.  vals may be null (keys only).  Passes whose digit is shared by
 // every key are skipped.  Must be called by all kSortThreads threads.
 template <int T, typename K, typename V>
-__device__ int cta_radix_sort(K *ka, K *kb, V *va, V *vb, int n, int bits, SortSmemT<T> &sm) {
+__device__ int cta_radix_sort(K *ka, K *kb, V *va, V *vb, int n, int bits, SortSmemT<T> &sm,
+                              int shift0 = 0) {
     constexpr int kSortWarps = T / 32, kSortThreads = T, kSortTile = T * kSortItems;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
     int parity = 0;
     K *src = ka, *dst = kb;
     V *vsrc = va, *vdst = vb;
-    for (int shift = 0; shift < bits; shift += 8) {
+    for (int shift = shift0; shift < shift0 + bits; shift += 8) {
         // ---- histogram
         for (int e = tid; e < kSortWarps * 256; e += kSortThreads) (&sm.wcnt[0][0])[e] = 0;
         if (tid == 0) sm.single = 0;

@@ -162,8 +162,31 @@ __global__ void __launch_bounds__(T) te_reduce_kernel(
         if (threadIdx.x == 0) out_te[blockIdx.x] = __longlong_as_double(0x7FF8000000000000ll);
         return;
     }
-    const int parity = cta_radix_sort<T, uint64_t, int>(src, dst, nullptr, nullptr, n, 64, sm);
-    const double sum = pairwise_cta(parity ? dst : src, n, parity ? src : dst, &n_leaves);
+    // stable sort on the high 32 key bits (sign, exponent, 20 mantissa bits),
+    // then every run of equal high halves is finished by an insertion sort on
+    // the full key: runs are almost always one value or copies of one value
+    // (equal brackets of equal count triples), so this halves the radix passes
+    const int parity = cta_radix_sort<T, uint64_t, int>(src, dst, nullptr, nullptr, n, 32, sm, 32);
+    uint64_t *sorted = parity ? dst : src;
+    for (int i = threadIdx.x; i < n; i += T) {
+        const uint32_t h = (uint32_t)(sorted[i] >> 32);
+        if ((i > 0 && (uint32_t)(sorted[i - 1] >> 32) == h) || i + 1 >= n ||
+            (uint32_t)(sorted[i + 1] >> 32) != h)
+            continue;  // not the start of a run of length >= 2
+        int e = i + 1;
+        while (e < n && (uint32_t)(sorted[e] >> 32) == h) ++e;
+        for (int a = i + 1; a < e; ++a) {
+            const uint64_t key = sorted[a];
+            int b = a - 1;
+            while (b >= i && sorted[b] > key) {
+                sorted[b + 1] = sorted[b];
+                --b;
+            }
+            sorted[b + 1] = key;
+        }
+    }
+    __syncthreads();
+    const double sum = pairwise_cta(sorted, n, parity ? src : dst, &n_leaves);
     if (threadIdx.x == 0) out_te[blockIdx.x] = __dadd_rn(psi_k, __ddiv_rn(sum, (double)n));
 }
 

@@ -166,3 +166,27 @@ def test_analyze_windows_equals_per_window_analyze_pair():
                               n_surrogates=20, seed=3)
     assert batch[1].te_value == ref["te_value"]
     assert batch[1].surrogate_values.tolist() == list(ref["surrogate_values"])
+
+
+def test_te_reduce_runs_of_equal_high_key_bits():
+    """Brackets that agree in their top 32 bits but differ below (the sort's
+    fix-up path) still reduce to numpy's exact sorted pairwise mean."""
+    import torch
+    from paper_1401_4068_b200 import _native as nat
+    rng = np.random.default_rng(9)
+    m = 3000
+    table = 1.0 + np.arange(64) * 2.0 ** -44           # values 1 ulp-ish apart at 2^-44
+    table[::7] = -0.5 - np.arange(10) * 2.0 ** -41     # and a few negative clusters
+    a, b, c = (rng.integers(0, 64, m).astype(np.int32) for _ in range(3))
+    vals = (table[a] - table[b]) - table[c]
+    ref = np.float64(0.25) + np.sort(vals).sum() / m    # numpy pairwise sum of the sorted terms
+    dev = nat.device()
+    counts = torch.from_numpy(np.stack([a, b, c])).to(dev)
+    psi = torch.from_numpy(table).to(dev)
+    out = torch.empty(1, dtype=torch.float64, device=dev)
+    L = nat.lib()
+    tab = nat.chunk_table([0], [m])
+    ws = nat.workspace(L.ente_te_reduce_workspace_size(tab, 1))
+    nat.check(L.ente_te_reduce(nat.ptr(counts), m, tab, 1, nat.ptr(psi), psi.numel(), 0.25,
+                               nat.ptr(out), nat.ptr(ws), ws.numel(), nat.stream_handle()), "reduce")
+    assert float(out.cpu()[0]) == float(ref)
