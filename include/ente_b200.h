@@ -87,6 +87,23 @@ int ente_search(const double *pts64, int64_t total_rows, int dim, const ente_chu
                void *stream);
 
 /* ---------------------------------------------------------------------------
+ * ente_search_split -- ente_search for part `split_index` of `split_count`:
+ * every chunk's references (in the search's own spatial order) are cut into
+ * split_count contiguous tile ranges and only this part's references get
+ * kth_distance / counts written; all other output rows are left untouched.
+ *
+ * The multi-GPU path for fewer chunks than GPUs: every rank
+ * runs the same chunks with its own split_index into zeroed outputs, and
+ * one sum all-reduce (exact: x + 0 = x) assembles the full result.  The
+ * parts are deterministic, disjoint and cover every row; both sweeps stay in
+ * one spatial order so each part is self-contained.
+ * ------------------------------------------------------------------------- */
+int ente_search_split(const double *pts64, int64_t total_rows, int dim, const ente_chunk *chunks,
+                      int n_chunks, const uint32_t *marg_masks, int n_marg, int k,
+                      int split_index, int split_count, double *out_eps, int32_t *out_counts,
+                      int32_t *status, void *workspace, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
  * ente_knn_indices -- the k nearest neighbours of every point, in the
  * canonical order ascending (fp64 max-norm distance, chunk-local index).
  *

@@ -47,6 +47,8 @@ def _declare(L):
         "ente_search": ([vp, i64, i32, cp, i32, u32p, i32, i32, vp, vp, vp, vp, sz, vp], i32),
         "ente_ragwitz_errors": ([vp, i32, i32, i32, i32, vp, vp, i32, i32, vp, vp], i32),
         "ente_knn_indices": ([vp, i64, i32, cp, i32, i32, vp, vp, vp, vp, sz, vp], i32),
+        "ente_search_split": ([vp, i64, i32, cp, i32, u32p, i32, i32, i32, i32, vp, vp, vp, vp, sz,
+                               vp], i32),
         "ente_radius_counts_workspace_size": ([i32], sz),
         "ente_radius_counts": ([vp, i64, i32, cp, i32, u32p, i32, vp, vp, vp, vp, sz, vp], i32),
         "ente_jitter_workspace_size": ([i32, i32], sz),

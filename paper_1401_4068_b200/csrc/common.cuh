@@ -32,7 +32,7 @@ struct ChunkInfo {
     int32_t npad;   // n rounded up to kTJ (pad rows hold +inf)
     double delta;   // |d32 - d64| bound (set by prep)
     int32_t ok32;   // fp32 filter usable for this chunk
-    int32_t pad_;
+    int32_t tile_lo;  // first sweep tile of this call's reference range (split searches)
 };
 
 struct TileRef {

@@ -272,13 +272,14 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double *__rest
 // principal axes of every chunk large enough to use them (one thread per
 // chunk; the serial power iteration stays out of the prep CTAs)
 __global__ void __launch_bounds__(128) axes_kernel(const ChunkInfo *__restrict__ info, int n_chunks,
-                                                   int dim, ColStats *__restrict__ stats) {
+                                                   int dim, ColStats *__restrict__ stats,
+                                                   int allow_pca) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= n_chunks) return;
     const ChunkInfo ci = info[c];
     ColStats &cs = stats[c];
     cs.use_pca = 0;
-    if (!ci.ok32 || ci.n < kPcaMinRows) return;
+    if (!allow_pca || !ci.ok32 || ci.n < kPcaMinRows) return;
     const int P = dim < kPcaCols ? dim : kPcaCols;
     // covariance about the mean from the moments about the first row
     double cov[kPcaCols][kPcaCols], d[kPcaCols];
@@ -539,7 +540,9 @@ __global__ void __launch_bounds__(kTJ) gather_kernel(const double *__restrict__ 
 // ---------------------------------------------------------------------------
 // sweep tile t -> (chunk, first sorted reference): tile0[c] = first tile of
 // chunk c (ascending, n_chunks + 1 entries); chunks without tiles repeat
-// their successor's value, so the largest c with tile0[c] <= t is the owner
+// their successor's value, so the largest c with tile0[c] <= t is the owner.
+// tile0[n_chunks + 1 + c] = the chunk's first tile index within the chunk
+// (non-zero only for split searches, which sweep a range of references).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ TileRef tile_of(const int32_t *__restrict__ tile0, int n_chunks, int t) {
     int lo = 0, hi = n_chunks - 1;
@@ -550,7 +553,7 @@ __device__ __forceinline__ TileRef tile_of(const int32_t *__restrict__ tile0, in
     }
     TileRef tr;
     tr.chunk = lo;
-    tr.r0 = (t - __ldg(tile0 + lo)) * kWarpRefs;
+    tr.r0 = (t - __ldg(tile0 + lo) + __ldg(tile0 + n_chunks + 1 + lo)) * kWarpRefs;
     return tr;
 }
 
@@ -1929,7 +1932,7 @@ static SearchWs layout_ws(Arena &a, const Plan &p, int n_chunks) {
     w.rs_n = w.ovf_n ? w.ovf_n + 1 : nullptr;
     if (p.fast) {
         w.stats = a.take<ColStats>(n_chunks);
-        w.tile0 = a.take<int32_t>(n_chunks + 1);
+        w.tile0 = a.take<int32_t>(2 * n_chunks + 1);
         w.pts32 = a.take<float>((size_t)p.total_prows * p.dp);
         w.fbox = a.take<float>((size_t)(p.total_prows / kSub) * 2 * kGate);
         w.ka = a.take<uint32_t>(p.total_rows);
@@ -2031,12 +2034,14 @@ static int validate(const ente_chunk *chunks, int n_chunks, int dim, const uint3
 
 // prep -> principal axes -> both sort orders -> both fp32 copies with boxes
 static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Plan &p,
-                         const SearchWs &w, int n_chunks, int32_t *status, int prune) {
+                         const SearchWs &w, int n_chunks, int32_t *status, int prune,
+                         int allow_pca = 1) {
         ENTE_LAUNCH("prep", st,
                     prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, w.stats, status, 1));
         ENTE_CUDA(cudaGetLastError());
         ENTE_LAUNCH("axes", st,
-                    axes_kernel<<<(n_chunks + 127) / 128, 128, 0, st>>>(w.info, n_chunks, dim, w.stats));
+                    axes_kernel<<<(n_chunks + 127) / 128, 128, 0, st>>>(w.info, n_chunks, dim, w.stats,
+                                                                        allow_pca));
         ENTE_CUDA(cudaGetLastError());
         FilterCols sfc = p.fc;
         if (!prune) sfc.nf = 0;  // identity order
@@ -2068,10 +2073,11 @@ static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Pl
 // host chunk table + status (K_TOO_LARGE) + per-chunk first sweep tile
 static int upload_chunks(cudaStream_t st, const ente_chunk *chunks, int n_chunks, int k,
                          const Plan &p, const SearchWs &w, int32_t *status,
-                         std::vector<int32_t> &htile0, int32_t &ntiles) {
+                         std::vector<int32_t> &htile0, int32_t &ntiles, int split_index = 0,
+                         int split_count = 1) {
     std::vector<ChunkInfo> hinfo(n_chunks);
     std::vector<int32_t> hstatus(n_chunks, ENTE_CHUNK_OK);
-    htile0.assign(n_chunks + 1, 0);
+    htile0.assign(2 * n_chunks + 1, 0);
     ntiles = 0;
     int64_t prow = 0;
     for (int c = 0; c < n_chunks; ++c) {
@@ -2082,10 +2088,17 @@ static int upload_chunks(cudaStream_t st, const ente_chunk *chunks, int n_chunks
         ci.prow0 = prow;
         ci.delta = 0.0;
         ci.ok32 = 0;
+        ci.tile_lo = 0;
         prow += ci.npad;
         if (k > ci.n - 1) hstatus[c] = ENTE_CHUNK_K_TOO_LARGE;
         htile0[c] = ntiles;
-        if (p.fast && hstatus[c] == ENTE_CHUNK_OK) ntiles += (ci.n + kWarpRefs - 1) / kWarpRefs;
+        // this call's share of the chunk's sweep tiles (all of them unless split)
+        const int64_t all = (ci.n + kWarpRefs - 1) / kWarpRefs;
+        const int lo = (int)(all * split_index / split_count);
+        const int hi = (int)(all * (split_index + 1) / split_count);
+        ci.tile_lo = lo;
+        htile0[n_chunks + 1 + c] = lo;
+        if (p.fast && hstatus[c] == ENTE_CHUNK_OK) ntiles += hi - lo;
     }
     htile0[n_chunks] = ntiles;
     ENTE_CUDA(cudaMemcpyAsync(w.info, hinfo.data(), sizeof(ChunkInfo) * n_chunks,
@@ -2142,10 +2155,10 @@ static unsigned long long *device_work() {
     return g_dwork[dev];
 }
 
-extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
-                           const ente_chunk *chunks, int n_chunks, const uint32_t *marg_masks,
-                           int n_marg, int k, double *out_eps, int32_t *out_counts,
-                           int32_t *status, void *workspace, size_t ws_bytes, void *stream) {
+static int search_impl(const double *pts64, int64_t total_rows, int dim, const ente_chunk *chunks,
+                       int n_chunks, const uint32_t *marg_masks, int n_marg, int k, double *out_eps,
+                       int32_t *out_counts, int32_t *status, void *workspace, size_t ws_bytes,
+                       void *stream, int split_index, int split_count) {
     int rc = validate(chunks, n_chunks, dim, marg_masks, n_marg, k);
     if (rc != ENTE_OK) return rc;
     if (n_chunks == 0) return ENTE_OK;
@@ -2166,7 +2179,8 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
     // host-side chunk table, tile list and k checks
     std::vector<int32_t> htile0;
     int32_t ntiles = 0;
-    rc = upload_chunks(st, chunks, n_chunks, k, p, w, status, htile0, ntiles);
+    rc = upload_chunks(st, chunks, n_chunks, k, p, w, status, htile0, ntiles, split_index,
+                       split_count);
     if (rc != ENTE_OK) return rc;
     Masks masks{};
     masks.n = n_marg;
@@ -2178,9 +2192,11 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
             set_error("ente_search: cannot allocate the work counters");
             return ENTE_ERR_CUDA;
         }
-        rc = launch_orders(st, pts64, dim, p, w, n_chunks, status, prune);
+        // a split search keeps both sweeps in the count order, so every rank's
+        // kNN pass covers exactly the references its count pass needs
+        rc = launch_orders(st, pts64, dim, p, w, n_chunks, status, prune, split_count == 1);
         if (rc != ENTE_OK) return rc;
-        ENTE_CUDA(cudaMemcpyAsync(w.tile0, htile0.data(), sizeof(int32_t) * (n_chunks + 1),
+        ENTE_CUDA(cudaMemcpyAsync(w.tile0, htile0.data(), sizeof(int32_t) * (2 * n_chunks + 1),
                                   cudaMemcpyHostToDevice, st));
         const unsigned nt = (unsigned)ntiles;
         ENTE_LAUNCH("knn_pass", st,
@@ -2212,7 +2228,7 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
         dispatch_exact(k, st, pts64, dim, w.info, n_chunks, status, w.ovf, w.ovf_n, 0, masks,
                        total_rows, out_eps, out_counts);
         ENTE_CUDA(cudaGetLastError());
-    } else if (!p.fast) {
+    } else if (!p.fast && split_index == 0) {  // (a split search: part 0 does it all)
         ENTE_LAUNCH("prep", st,
                     prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, nullptr, status, 0));
         ENTE_CUDA(cudaGetLastError());
@@ -2221,6 +2237,27 @@ extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
         ENTE_CUDA(cudaGetLastError());
     }
     return ENTE_OK;
+}
+
+extern "C" int ente_search(const double *pts64, int64_t total_rows, int dim,
+                           const ente_chunk *chunks, int n_chunks, const uint32_t *marg_masks,
+                           int n_marg, int k, double *out_eps, int32_t *out_counts,
+                           int32_t *status, void *workspace, size_t ws_bytes, void *stream) {
+    return search_impl(pts64, total_rows, dim, chunks, n_chunks, marg_masks, n_marg, k, out_eps,
+                       out_counts, status, workspace, ws_bytes, stream, 0, 1);
+}
+
+extern "C" int ente_search_split(const double *pts64, int64_t total_rows, int dim,
+                                 const ente_chunk *chunks, int n_chunks,
+                                 const uint32_t *marg_masks, int n_marg, int k, int split_index,
+                                 int split_count, double *out_eps, int32_t *out_counts,
+                                 int32_t *status, void *workspace, size_t ws_bytes, void *stream) {
+    if (split_count < 1 || split_index < 0 || split_index >= split_count) {
+        set_error("ente_search_split: split %d of %d", split_index, split_count);
+        return ENTE_ERR_ARG;
+    }
+    return search_impl(pts64, total_rows, dim, chunks, n_chunks, marg_masks, n_marg, k, out_eps,
+                       out_counts, status, workspace, ws_bytes, stream, split_index, split_count);
 }
 
 // Evaluated (reference, candidate) pairs (whole sub-tiles x reference groups) of the two sweeps on the

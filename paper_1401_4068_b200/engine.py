@@ -81,7 +81,7 @@ def column_mask(cols, dim: int) -> int:
 # device-level entry points (tensors in, tensors out; used by ksg / bench)
 # ---------------------------------------------------------------------------
 def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int, reuse: bool = False,
-                  tag: str = ""):
+                  tag: str = "", split=None):
     """ente_search on a device-resident [rows, dim] fp64 matrix.
 
     Returns (eps [rows] f64, counts [n_marg, rows] int32, status [n_chunks] int32),
@@ -104,9 +104,17 @@ def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int, reuse: bool = F
         status = torch.empty(max(1, len(ns)), dtype=torch.int32, device=pts64.device)
     need = L.ente_search_workspace_size(table, len(ns), dim, len(masks), int(k))
     ws = nat.workspace(need, tag)
-    nat.check(L.ente_search(nat.ptr(pts64), rows, dim, table, len(ns), marr, len(masks), int(k),
-                            nat.ptr(eps), nat.ptr(counts), nat.ptr(status), nat.ptr(ws), ws.numel(),
-                            nat.stream_handle()), "ente_search")
+    if split is None:
+        nat.check(L.ente_search(nat.ptr(pts64), rows, dim, table, len(ns), marr, len(masks),
+                                int(k), nat.ptr(eps), nat.ptr(counts), nat.ptr(status),
+                                nat.ptr(ws), ws.numel(), nat.stream_handle()), "ente_search")
+    else:  # (index, count): this part's references only, other rows zeroed
+        eps.zero_()
+        counts.zero_()
+        nat.check(L.ente_search_split(nat.ptr(pts64), rows, dim, table, len(ns), marr, len(masks),
+                                      int(k), int(split[0]), int(split[1]), nat.ptr(eps),
+                                      nat.ptr(counts), nat.ptr(status), nat.ptr(ws), ws.numel(),
+                                      nat.stream_handle()), "ente_search_split")
     return eps, counts[:len(masks)], status[:len(ns)]
 
 

@@ -68,3 +68,33 @@ def test_sharded_run_gloo_world2(tmp_path):
     res = np.load(out)
     assert np.array_equal(res["te"], _te_of(_items()))
     assert res["gathered"].tolist() == [0.0, 0.0, 1.0]
+
+
+@pytest.mark.gpu
+def test_analyze_pairs_distributed_equals_analyze_pairs(tmp_path):
+    """Single-rank process group on the GPU: the sharded multi-pair analysis
+    reproduces analyze_pairs bit for bit (placement never changes a TE)."""
+    from paper_1401_4068_b200 import workloads
+    from paper_1401_4068_b200.data import AnalysisConfig, EmbeddingSpec, EnsembleSeries
+    from paper_1401_4068_b200.inference import analyze_pairs
+    from paper_1401_4068_b200.scheduler import analyze_pairs_distributed
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        series = {}
+        for p in range(3):
+            x, y = workloads.ar_pair("bidirectional", 30, 300, seed=p)
+            series[f"X{p}"] = EnsembleSeries(f"X{p}", x)
+            series[f"Y{p}"] = EnsembleSeries(f"Y{p}", y)
+        pairs = [(f"X{p}", f"Y{p}") for p in range(3)] + [("Y0", "X0")]
+        specs = {k: EmbeddingSpec(2, 1) for k in series}
+        cfg = AnalysisConfig(u_candidates=(5, 7), window=(200, 230), k=4, n_surrogates=15,
+                             seed=2, correction="fdr")
+        ref = analyze_pairs(series, pairs, specs, cfg)
+        got = analyze_pairs_distributed(series, pairs, specs, cfg, dist)
+        for a, b in zip(ref, got):
+            assert (a.te_value, a.p_value, a.u_selected) == (b.te_value, b.p_value, b.u_selected)
+            assert a.surrogate_values.tolist() == b.surrogate_values.tolist()
+            assert a.significant_corrected == b.significant_corrected
+    finally:
+        dist.destroy_process_group()

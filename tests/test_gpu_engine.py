@@ -232,3 +232,53 @@ def test_knn_indices_large_pruned_chunk():
     for row, i in enumerate(sel):
         order = np.lexsort((np.arange(n), d[row]))[:4]
         assert np.array_equal(got[i], order)
+
+
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_split_search_parts_cover_every_row_once(parts):
+    """ente_search_split: the parts' outputs are disjoint and sum to the full search."""
+    import torch
+    from paper_1401_4068_b200.engine import search_device
+    rng = np.random.default_rng(parts)
+    chunks = [rng.standard_normal((7000, 7)), np.round(rng.standard_normal((3000, 7)), 1),
+              rng.standard_normal((200, 7))]
+    ns = np.array([len(c) for c in chunks])
+    rows0 = np.concatenate([[0], np.cumsum(ns)[:-1]])
+    dev = torch.from_numpy(np.concatenate(chunks)).cuda()
+    margs = cases.te_margs(3, 3)
+    masks = [sum(1 << c for c in m) for m in margs]
+    eps_sum = torch.zeros(dev.shape[0], dtype=torch.float64, device=dev.device)
+    cnt_sum = torch.zeros((3, dev.shape[0]), dtype=torch.int32, device=dev.device)
+    written = torch.zeros(dev.shape[0], dtype=torch.int32, device=dev.device)
+    for part in range(parts):
+        eps, cnt, _ = search_device(dev, rows0, ns, masks, 4, split=(part, parts))
+        eps_sum += eps
+        cnt_sum += cnt
+        written += (eps != 0).int()
+    assert int(written.max()) <= 1
+    for c, r0, n in zip(chunks, rows0, ns):
+        e, cnt = oracle.search(c, margs, 4)
+        assert np.array_equal(eps_sum[r0:r0 + n].cpu().numpy(), e)
+        for m in range(3):
+            assert np.array_equal(cnt_sum[m, r0:r0 + n].cpu().numpy().astype(np.int64), cnt[m])
+
+
+def test_batch_search_split_single_rank_group():
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1401_4068_b200.scheduler import batch_search_split
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        pts = np.random.default_rng(4).standard_normal((5000, 5))
+        margs = cases.te_margs(2, 2)
+        (r,) = batch_search_split([(Chunk(pts), margs)], 4, dist)
+        e, c = oracle.search(pts, margs, 4)
+        assert np.array_equal(r.kth_distance, e)
+        assert all(np.array_equal(a, b) for a, b in zip(r.radius_counts, c))
+    finally:
+        dist.destroy_process_group()
