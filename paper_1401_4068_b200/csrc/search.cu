@@ -42,7 +42,11 @@ namespace ente {
 // ---------------------------------------------------------------------------
 // prep: column statistics, error bound, finiteness
 // ---------------------------------------------------------------------------
-constexpr int kSub = 32;                    // candidate rows per sub-tile (one TMA copy)
+#ifndef ENTE_KSUB
+#define ENTE_KSUB 32
+#endif
+constexpr int kSub = ENTE_KSUB;             // candidate rows per sub-tile (one TMA copy); 16 or 32
+static_assert(kSub == 16 || kSub == 32, "sub-tiles are half or whole warps of rows");
 constexpr int kWarpRefs = 32 * kRT;         // references per sweep CTA (one warp)
 constexpr int kGate = 4;                    // gate columns in the Morton key and the boxes
 // minimum resident sweep CTAs (one warp each) per SM: caps the registers
@@ -451,7 +455,7 @@ __global__ void __launch_bounds__(kTJ) gather_knn_kernel(
         if (valid) kmap[ci.row0 + s] = inv[orig];
         float4 *q4 = reinterpret_cast<float4 *>(pts32 + (ci.prow0 + s) * dp);
         float4 quad = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int64_t sub = ci.prow0 / kSub + stage * (kTJ / kSub) + warp;
+        const int64_t sub = ci.prow0 / kSub + stage * (kTJ / kSub) + warp * (32 / kSub) + lane / kSub;
         for (int col = 0; col < dp; ++col) {
             float v = 0.0f;
             if (col < dim)
@@ -464,18 +468,18 @@ __global__ void __launch_bounds__(kTJ) gather_knn_kernel(
                     lo = valid ? v : INFINITY;
                     hi = valid ? v : -INFINITY;
 #pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) {
+                    for (int off = kSub / 2; off > 0; off >>= 1) {
                         lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
                         hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, off));
                     }
                 }
-                if (lane == 0) {
+                if (lane % kSub == 0) {
                     fbox[sub * 2 * NB + col] = lo;
                     fbox[sub * 2 * NB + NB + col] = hi;
                 }
             }
         }
-        if (lane == 0)
+        if (lane % kSub == 0)
             for (int col = dp; col < NB; ++col) fbox[sub * 2 * NB + col] = fbox[sub * 2 * NB + NB + col] = 0.0f;
     }
 }
@@ -505,7 +509,7 @@ __global__ void __launch_bounds__(kTJ) gather_kernel(const double *__restrict__ 
         if (valid && inv) inv[orig] = s;
         float4 *q4 = reinterpret_cast<float4 *>(pts32 + (ci.prow0 + s) * dp);
         float4 quad = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int64_t sub = ci.prow0 / kSub + stage * (kTJ / kSub) + warp;
+        const int64_t sub = ci.prow0 / kSub + stage * (kTJ / kSub) + warp * (32 / kSub) + lane / kSub;
         for (int col = 0; col < dp; ++col) {
             float v = 0.0f;
             if (col < dim)
@@ -519,19 +523,19 @@ __global__ void __launch_bounds__(kTJ) gather_kernel(const double *__restrict__ 
                     lo = valid ? v : INFINITY;
                     hi = valid ? v : -INFINITY;
 #pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) {
+                    for (int off = kSub / 2; off > 0; off >>= 1) {
                         lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
                         hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, off));
                     }
                 }
-                if (lane == 0) {
+                if (lane % kSub == 0) {
                     fbox[sub * 2 * kGate + g] = lo;
                     fbox[sub * 2 * kGate + kGate + g] = hi;
                 }
             }
         }
         // gate slots beyond the columns (dim < f0 + kGate)
-        if (lane == 0)
+        if (lane % kSub == 0)
             for (int g = dim - fc.f0; g < kGate; ++g)
                 if (g >= 0) fbox[sub * 2 * kGate + g] = fbox[sub * 2 * kGate + kGate + g] = 0.0f;
     }
@@ -1448,14 +1452,14 @@ __global__ void __launch_bounds__(kRescanWarps * 32) rescan_kernel(
                 const int st = base + __ffs(m) - 1;
                 m &= m - 1;
                 const int j = st * kSub + lane;
-                const float *q = cp + (int64_t)j * DP;
+                const float *q = cp + (int64_t)(lane < kSub ? j : st * kSub) * DP;
                 float d = 0.0f;
 #pragma unroll
                 for (int col = 0; col < D; ++col) {
                     const float x = (col & 1) ? ref[col >> 1].y : ref[col >> 1].x;
                     d = fmaxf(d, fabsf(q[col] + x));
                 }
-                if (j < ci.n && j != s && d <= hiA) {
+                if (lane < kSub && j < ci.n && j != s && d <= hiA) {
                     const double *q64 = pts64 + (ci.row0 + perm[ci.row0 + j]) * D;
                     double d64 = 0.0;
 #pragma unroll
@@ -1496,7 +1500,7 @@ __global__ void __launch_bounds__(kRescanWarps * 32) rescan_kernel(
                 const int st = base + __ffs(m) - 1;
                 m &= m - 1;
                 const int j = st * kSub + lane;
-                if (j >= ci.n || j == s) continue;
+                if (lane >= kSub || j >= ci.n || j == s) continue;
                 const float *q = cp + (int64_t)j * DP;
                 float a = 0.0f, b = 0.0f;
 #pragma unroll
@@ -1717,7 +1721,7 @@ __global__ void __launch_bounds__(kIdxWarps * 32) knn_index_kernel(
                     const int st = base + __ffs(m) - 1;
                     m &= m - 1;
                     const int j = st * kSub + lane;
-                    if (j >= ci.n || j == s) continue;
+                    if (lane >= kSub || j >= ci.n || j == s) continue;
                     const float *q32 = cp + (int64_t)j * DP;
                     float d = 0.0f;
 #pragma unroll
