@@ -36,40 +36,13 @@
 #include "common.cuh"
 #include "profile.cuh"
 #include "radix.cuh"
+#include "sweeps.cuh"
 
 namespace ente {
 
 // ---------------------------------------------------------------------------
 // prep: column statistics, error bound, finiteness
 // ---------------------------------------------------------------------------
-#ifndef ENTE_KSUB
-#define ENTE_KSUB 32
-#endif
-constexpr int kSub = ENTE_KSUB;             // candidate rows per sub-tile (one TMA copy); 16 or 32
-static_assert(kSub == 16 || kSub == 32, "sub-tiles are half or whole warps of rows");
-constexpr int kWarpRefs = 32 * kRT;         // references per sweep CTA (one warp)
-constexpr int kGate = 4;                    // gate columns in the Morton key and the boxes
-// minimum resident sweep CTAs (one warp each) per SM: caps the registers
-#ifndef ENTE_KNN_NSLOT
-#define ENTE_KNN_NSLOT 4
-#endif
-#ifndef ENTE_CNT_NSLOT
-#define ENTE_CNT_NSLOT 2
-#endif
-#ifndef ENTE_CNT_MINB
-#define ENTE_CNT_MINB 32
-#endif
-#ifndef ENTE_KNN_MINB
-#define ENTE_KNN_MINB 32
-#endif
-// resident one-warp sweep CTAs per SM by layout width: 32 (64 registers)
-// up to D = 7, fewer for wider layouts so their references stay in registers
-__host__ __device__ constexpr int sweep_minb(int D, int cap) {
-    return D <= 7 ? cap : (D <= 9 ? (cap < 28 ? cap : 28) : (D <= 11 ? (cap < 24 ? cap : 24)
-                                                              : (D <= 13 ? (cap < 20 ? cap : 20) : 16)));
-}
-constexpr int kKnnQ = 2;                    // kNN sub-tile boxes: 4 * kKnnQ columns from 0
-
 // fp32 row writer of the gathers: columns are collected in a float4 register
 // and written as one 16-byte store per quad (rows are 16-B aligned, D padded
 // to a multiple of 4) instead of one 4-byte store per column
@@ -541,787 +514,6 @@ __global__ void __launch_bounds__(kTJ) gather_kernel(const double *__restrict__ 
     }
 }
 
-// ---------------------------------------------------------------------------
-// sweep tile t -> (chunk, first sorted reference): tile0[c] = first tile of
-// chunk c (ascending, n_chunks + 1 entries); chunks without tiles repeat
-// their successor's value, so the largest c with tile0[c] <= t is the owner.
-// tile0[n_chunks + 1 + c] = the chunk's first tile index within the chunk
-// (non-zero only for split searches, which sweep a range of references).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ TileRef tile_of(const int32_t *__restrict__ tile0, int n_chunks, int t) {
-    int lo = 0, hi = n_chunks - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(tile0 + mid) <= t) lo = mid;
-        else hi = mid - 1;
-    }
-    TileRef tr;
-    tr.chunk = lo;
-    tr.r0 = (t - __ldg(tile0 + lo) + __ldg(tile0 + n_chunks + 1 + lo)) * kWarpRefs;
-    return tr;
-}
-
-// ---------------------------------------------------------------------------
-// register-level helpers for the fp32 sweeps
-// TE layout columns: 0 = y_t, 1..DY = y-past, DY+1..D-1 = x-past
-// (embedding.py:50-60).  Coordinates are held as packed pairs (0,1), (2,3)...
-// so one FADD2 gives two differences.  Pairs [0, PG) cover columns 0..DY
-// (the gate: y-past plus y_t), pairs [PG, NP) the rest.
-// ---------------------------------------------------------------------------
-template <int DY, int DX>
-struct Lay {
-    static constexpr int D = 1 + DY + DX;
-    static constexpr int DP = (D + 3) & ~3;
-    static constexpr int NP = (D + 1) / 2;     // coordinate pairs
-    static constexpr int PG = (DY + 2) / 2;    // gate pairs: columns 0 .. 2*PG-1 >= DY
-    static constexpr int NSLOT = DP <= 8 ? 8 : (DP <= 12 ? 6 : 4);  // ring slots per warp
-};
-
-template <int D>
-__device__ __forceinline__ void load_ref(float2 (&nr)[(D + 1) / 2], const float *__restrict__ row,
-                                         bool valid) {
-#pragma unroll
-    for (int p = 0; p < (D + 1) / 2; ++p) {
-        const float a = valid ? row[2 * p] : 0.0f;
-        const float b = (valid && 2 * p + 1 < D) ? row[2 * p + 1] : 0.0f;
-        nr[p] = make_float2(-a, -b);
-    }
-}
-
-// difference pairs [P0, P1) of ref (negated, packed) and candidate row (smem)
-template <int D, int P0, int P1>
-__device__ __forceinline__ void diff_pairs(const float2 (&nr)[(D + 1) / 2], const float2 *c,
-                                           float (&a)[2 * ((D + 1) / 2)]) {
-#pragma unroll
-    for (int p = P0; p < P1; ++p) {
-        if (2 * p + 1 < D) {
-            const float2 d = __fadd2_rn(nr[p], c[p]);
-            a[2 * p] = d.x;
-            a[2 * p + 1] = d.y;
-        } else {
-            a[2 * p] = nr[p].x + c[p].x;
-        }
-    }
-}
-
-// max |a[c]| for c in [LO, HI) folded into acc (3-input FMNMX chain)
-template <int LO, int HI, int N>
-__device__ __forceinline__ float maxabs(const float (&a)[N], float acc) {
-    int c = LO;
-#pragma unroll
-    for (; c + 1 < HI; c += 2) acc = fmaxf(fmaxf(acc, fabsf(a[c])), fabsf(a[c + 1]));
-    if (c < HI) acc = fmaxf(acc, fabsf(a[c]));
-    return acc;
-}
-
-template <int LO, int HI, int N>
-__device__ __forceinline__ float maxabs0(const float (&a)[N]) {
-    if constexpr (HI - LO <= 0) return 0.0f;
-    else if constexpr (HI - LO == 1) return fabsf(a[LO]);
-    else return maxabs<LO + 2, HI, N>(a, fmaxf(fabsf(a[LO]), fabsf(a[LO + 1])));
-}
-
-// Keep the S smallest values, ascending (new[s] = median(old[s-1], old[s], d));
-// a no-op when d >= kd[S-1].
-template <int S>
-__device__ __forceinline__ void insert_sorted(float (&kd)[S], float d) {
-#pragma unroll
-    for (int s = S - 1; s >= 1; --s) kd[s] = fmaxf(kd[s - 1], fminf(kd[s], d));
-    kd[0] = fminf(kd[0], d);
-}
-
-struct Band {
-    float nlo, nt;  // -lo, -t
-    float lo, hi, w;
-};
-
-__device__ __forceinline__ Band make_band(float t32, double delta) {
-    Band b;
-    const double two = 2.0 * delta;
-    const float lo = __double2float_rd(__dsub_rd((double)t32, two));
-    const float hi = __double2float_ru(__dadd_ru((double)t32, two));
-    const double w = fmax(__dsub_ru((double)t32, (double)lo), __dsub_ru((double)hi, (double)t32));
-    b.lo = lo;
-    b.hi = hi;
-    b.nlo = -lo;
-    b.nt = -t32;
-    b.w = __double2float_ru(w);
-    return b;
-}
-
-__device__ __forceinline__ float warp_max_nonneg(float v) {
-    return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(v, 0.0f))));
-}
-
-// ---------------------------------------------------------------------------
-// Warp-private candidate stream.
-//
-// Each sweep CTA is ONE warp owning 128 consecutive sorted references (4 per
-// lane).  It walks the chunk's 32-row sub-tiles home-first, then alternately
-// below and above (nearest first in the Morton order, so kNN bounds shrink
-// early).  Sub-tile boxes are tested 32 positions at a time, one per lane,
-// with the next window's boxes prefetched into registers; needed sub-tiles
-// are streamed into a ring of NSLOT shared-memory slots by the TMA engine
-// (cp.async.bulk + mbarrier).  Warps never wait for each other.
-// ---------------------------------------------------------------------------
-// A sub-tile box: Q float4 quads of column minima, then Q of maxima
-// (fbox layout per sub-tile: lo[4Q] | hi[4Q], float4 index st * 2Q).
-template <int Q>
-struct Box {
-    float4 lo[Q], hi[Q];
-};
-
-template <int Q>
-__device__ __forceinline__ Box<Q> load_box(const float4 *__restrict__ fb, int st) {
-    Box<Q> b;
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        b.lo[q] = __ldg(fb + 2 * Q * st + q);
-        b.hi[q] = __ldg(fb + 2 * Q * st + Q + q);
-    }
-    return b;
-}
-
-__device__ __forceinline__ float gap4(float4 lo, float4 hi, float4 blo, float4 bhi) {
-    const float a = fmaxf(fmaxf(lo.x - bhi.x, blo.x - hi.x), fmaxf(lo.y - bhi.y, blo.y - hi.y));
-    const float b = fmaxf(fmaxf(lo.z - bhi.z, blo.z - hi.z), fmaxf(lo.w - bhi.w, blo.w - hi.w));
-    return fmaxf(a, b);
-}
-
-template <int Q>
-struct Walker {
-    int h0, nh, nsub, npos;
-    int base;       // first position of the evaluated window (-32 before the first)
-    uint32_t mask;  // needed positions of that window not yet issued
-    int wst;        // per lane: sub-tile at position base + lane (-1: none)
-    float wd;       // per lane: its box distance
-    int nst;        // per lane: sub-tile at position base + 32 + lane (prefetched)
-    Box<Q> nb;      // its box
-    Box<Q> own;     // the warp's own box, identical in all lanes
-    uint32_t need;  // per lane: refs_need() bits of the sub-tile last returned
-
-    __device__ int sub_at(int pos) const {
-        if (pos < nh) return h0 + pos;
-        const int p = pos - nh, k = (p >> 1) + 1;
-        const int s = (p & 1) ? h0 + nh - 1 + k : h0 - k;
-        return (s >= 0 && s < nsub) ? s : -1;
-    }
-
-    __device__ void prefetch(const float4 *__restrict__ fb, int pos) {
-        nst = pos < npos ? sub_at(pos) : -1;
-        if (nst >= 0) nb = load_box<Q>(fb, nst);
-    }
-
-    __device__ void init(const float4 *__restrict__ fb, int wrow, int n, int npad) {
-        h0 = wrow / kSub;
-        nh = (min(wrow + 32 * kRT, n) - wrow + kSub - 1) / kSub;
-        nsub = npad / kSub;
-        npos = nh + 2 * max(h0, nsub - h0 - nh);
-        base = -32;
-        mask = 0;
-        own = load_box<Q>(fb, h0);
-        for (int s = 1; s < nh; ++s) {
-            const Box<Q> b = load_box<Q>(fb, h0 + s);
-#pragma unroll
-            for (int q = 0; q < Q; ++q) {
-                own.lo[q] = make_float4(fminf(own.lo[q].x, b.lo[q].x), fminf(own.lo[q].y, b.lo[q].y),
-                                        fminf(own.lo[q].z, b.lo[q].z), fminf(own.lo[q].w, b.lo[q].w));
-                own.hi[q] = make_float4(fmaxf(own.hi[q].x, b.hi[q].x), fmaxf(own.hi[q].y, b.hi[q].y),
-                                        fmaxf(own.hi[q].z, b.hi[q].z), fmaxf(own.hi[q].w, b.hi[q].w));
-            }
-        }
-        prefetch(fb, (threadIdx.x & 31));
-    }
-
-    // fp32 box distance (a lower bound of every d32 between the two boxes:
-    // fl is monotone, fl(x_j - x_i) >= fl(lo_j - hi_i))
-    __device__ float dist(const Box<Q> &b) const {
-        float d = 0.0f;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) d = fmaxf(d, gap4(b.lo[q], b.hi[q], own.lo[q], own.hi[q]));
-        return d;
-    }
-
-    // Next sub-tile whose box distance to the warp's box is below `bound`
-    // (strict) or not above it, AND that some reference of the warp needs by
-    // its own point-to-box distance (refs_need(box), evaluated per lane);
-    // returns -1 when the walk is over.
-    template <class RefTest>
-    __device__ int next(const float4 *__restrict__ fb, float bound, bool strict,
-                        RefTest &&refs_need) {
-        const int lane = threadIdx.x & 31;
-        for (;;) {
-            while (mask == 0) {
-                if (base + 32 >= npos) return -1;
-                base += 32;
-                wst = nst;
-                wd = wst >= 0 ? dist(nb) : INFINITY;
-                mask = __ballot_sync(0xffffffffu, strict ? (wd < bound) : (wd <= bound));
-                prefetch(fb, base + 32 + lane);
-            }
-            const int b = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const float d = __shfl_sync(0xffffffffu, wd, b);
-            if (!(strict ? (d < bound) : (d <= bound))) continue;  // the bound may have shrunk
-            const int st = __shfl_sync(0xffffffffu, wst, b);
-            const uint32_t nm = (uint32_t)refs_need(load_box<Q>(fb, st));
-            if (__any_sync(0xffffffffu, nm != 0u)) {
-                need = nm;
-                return st;
-            }
-        }
-    }
-};
-
-// fp32 distance from a reference (negated packed coordinates) to a sub-tile
-// box over the columns F0 .. F0 + NC - 1 (box slot g = column - F0): a lower
-// bound of the reference's fp32 distance to every row of the sub-tile over
-// any column set containing them (fl monotone).
-template <int F0, int NC, int NP, int Q>
-__device__ __forceinline__ float point_box(const float2 (&nr)[NP], const Box<Q> &b) {
-    float d = 0.0f;
-#pragma unroll
-    for (int g = 0; g < NC; ++g) {
-        const int c = F0 + g;  // column
-        const float x = (c & 1) ? nr[c >> 1].y : nr[c >> 1].x;  // -x_c
-        const float4 l4 = b.lo[g >> 2], h4 = b.hi[g >> 2];
-        const float l = (g & 3) == 0 ? l4.x : (g & 3) == 1 ? l4.y : (g & 3) == 2 ? l4.z : l4.w;
-        const float h = (g & 3) == 0 ? h4.x : (g & 3) == 1 ? h4.y : (g & 3) == 2 ? h4.z : h4.w;
-        const float2 e = __fadd2_rn(make_float2(l, h), make_float2(x, x));  // lo-x, hi-x
-        d = fmaxf(fmaxf(d, e.x), -e.y);
-    }
-    return d;
-}
-
-template <int DP, int NSLOT>
-struct Ring {
-    float buf[NSLOT][kSub * DP];
-    uint64_t full[NSLOT];
-};
-
-template <int DP, int NSLOT>
-__device__ __forceinline__ void ring_issue(Ring<DP, NSLOT> &ring, int slot, const float *src) {
-    constexpr uint32_t bytes = kSub * DP * sizeof(float);
-    fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&ring.full[slot], bytes);
-    bulk_g2s(ring.buf[slot], src, bytes, &ring.full[slot]);
-}
-
-// ---------------------------------------------------------------------------
-// pass 1: fp32 k-th neighbour distance (self included as the (k+1)-th slot)
-// lane l owns sorted rows wrow + r*32 + l, r < kRT
-// ---------------------------------------------------------------------------
-template <int DY, int DX, int S>
-__global__ void __launch_bounds__(32, S > 8 ? 16 : sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) knn_pass_kernel(
-    const float *__restrict__ pts32, const float *__restrict__ fbox,
-    const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks, int k, int prune,
-    const int32_t *__restrict__ kmap, float *__restrict__ t32_out, int32_t *__restrict__ L_out,
-    unsigned long long *__restrict__ work) {
-    using L = Lay<DY, DX>;
-    constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG;
-    constexpr int NSLOT = L::NSLOT < ENTE_KNN_NSLOT ? L::NSLOT : ENTE_KNN_NSLOT;
-    constexpr int NBC = D < 4 * kKnnQ ? D : 4 * kKnnQ;  // box columns 0 .. NBC-1
-    __shared__ __align__(128) Ring<DP, NSLOT> ring;
-    const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
-    const ChunkInfo ci = info[tr.chunk];
-    if (!ci.ok32) return;
-    const int lane = threadIdx.x;
-    const float *cp = pts32 + ci.prow0 * DP;
-    const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2 * kKnnQ;
-    const int wrow = tr.r0;
-    float2 ref[kRT][NP];
-    float kd[kRT][S];
-#pragma unroll
-    for (int r = 0; r < kRT; ++r) {
-        const int idx = wrow + r * 32 + lane;
-        const bool valid = idx < ci.n;
-        load_ref<D>(ref[r], cp + (int64_t)idx * DP, valid);
-#pragma unroll
-        for (int s = 0; s < S; ++s) kd[r][s] = (!valid || s < S - (k + 1)) ? -INFINITY : INFINITY;
-    }
-    if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
-    fence_barrier_init();
-    __syncwarp();
-    Walker<kKnnQ> wk;
-    wk.init(fb, wrow, ci.n, ci.npad);
-    float bound = INFINITY;  // warp max of the current k-th distances
-    auto refs_need = [&](const Box<kKnnQ> &b) {
-        bool need = !prune;
-#pragma unroll
-        for (int r = 0; r < kRT; ++r) need |= point_box<0, NBC, NP, kKnnQ>(ref[r], b) < kd[r][S - 1];
-        return need;
-    };
-    int slot_st = -1;        // lane s: sub-tile in ring slot s
-    int issued = 0;
-    uint32_t nsub = 0;
-    for (; issued < NSLOT; ++issued) {
-        const int st = wk.next(fb, prune ? bound : INFINITY, true, refs_need);
-        if (st < 0) break;
-        if (lane == issued) slot_st = st;
-        if (lane == 0) ring_issue(ring, issued, cp + (int64_t)st * kSub * DP);
-    }
-    for (int used = 0; used < issued; ++used) {
-        const int slot = used % NSLOT;
-        mbar_wait(&ring.full[slot], (uint32_t)(used / NSLOT) & 1u);
-        const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[slot]);
-        constexpr int G = 2 * PG < D ? 2 * PG : D;  // gate columns 0 .. G-1
-        constexpr int NQ = DP / 4;
-        float4 nxt[NQ];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) nxt[q] = tile[q];
-#pragma unroll 2
-        for (int j = 0; j < kSub; ++j) {
-            float4 cur[NQ];
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) cur[q] = nxt[q];
-            if (j + 1 < kSub) {  // prefetch the next candidate row
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) nxt[q] = tile[(j + 1) * NQ + q];
-            }
-            const float2 *c = reinterpret_cast<const float2 *>(cur);
-            float a[kRT][2 * NP];
-            float dj[kRT];
-            bool need = false;
-#pragma unroll
-            for (int r = 0; r < kRT; ++r) {
-                diff_pairs<D, 0, PG>(ref[r], c, a[r]);
-                dj[r] = maxabs0<0, G, 2 * NP>(a[r]);
-                need |= dj[r] < kd[r][S - 1];
-            }
-            if (__any_sync(0xffffffffu, need)) {
-                bool ins = false;
-#pragma unroll
-                for (int r = 0; r < kRT; ++r) {
-                    diff_pairs<D, PG, NP>(ref[r], c, a[r]);
-                    dj[r] = maxabs<G, D, 2 * NP>(a[r], dj[r]);
-                    ins |= dj[r] < kd[r][S - 1];
-                }
-                if (ins) {
-#pragma unroll
-                    for (int r = 0; r < kRT; ++r) insert_sorted<S>(kd[r], dj[r]);
-                }
-            }
-        }
-        ++nsub;
-        float wb = 0.0f;
-#pragma unroll
-        for (int r = 0; r < kRT; ++r) wb = fmaxf(wb, kd[r][S - 1]);
-        bound = warp_max_nonneg(wb);
-        __syncwarp();
-        const int st = wk.next(fb, prune ? bound : INFINITY, true, refs_need);
-        if (st >= 0) {
-            if (lane == issued % NSLOT) slot_st = st;
-            if (lane == 0) ring_issue(ring, issued % NSLOT, cp + (int64_t)st * kSub * DP);
-            ++issued;
-        }
-    }
-    (void)slot_st;
-    if (lane == 0) atomicAdd(work, (unsigned long long)nsub);
-#pragma unroll
-    for (int r = 0; r < kRT; ++r) {
-        const int idx = wrow + r * 32 + lane;
-        if (idx >= ci.n) continue;
-        const float t32 = kd[r][S - 1];
-        const float lo = __double2float_rd(__dsub_rd((double)t32, 2.0 * ci.delta));
-        int Lc = 0;
-#pragma unroll
-        for (int s = 0; s < S; ++s) Lc += (kd[r][s] > -INFINITY) && (kd[r][s] < lo);
-        if (lo > 0.0f) Lc -= 1;  // the self pair (distance 0) was counted
-        const int64_t orow = ci.row0 + (kmap ? kmap[ci.row0 + idx] : idx);  // count-order row
-        t32_out[orow] = t32;
-        L_out[orow] = Lc;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// pass 2, direct mapping (small chunks): two fixed references per lane
-//   marginal 0 = y-past (A), 1 = y + y-past (m2), 2 = y-past + x-past (m3)
-//   A <= every marginal and the joint, so A > hi settles a pair (outside
-//   everywhere, no event) after the gate columns alone
-// ---------------------------------------------------------------------------
-template <int DY, int DX>
-__global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) count_pass_direct_kernel(
-    const float *__restrict__ pts32, const float *__restrict__ fbox,
-    const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks,
-    const float *__restrict__ t32_in, int64_t ws_rows, int prune, int32_t *__restrict__ cnt_out,
-    uint32_t *__restrict__ ev, int32_t *__restrict__ ev_n, uint32_t fmask,
-    unsigned long long *__restrict__ work) {
-    using L = Lay<DY, DX>;
-    constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG, NSLOT = L::NSLOT;
-    __shared__ __align__(128) Ring<DP, NSLOT> ring;
-    const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
-    const ChunkInfo ci = info[tr.chunk];
-    if (!ci.ok32) return;
-    const int lane = threadIdx.x;
-    const float *cp = pts32 + ci.prow0 * DP;
-    const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2;
-    const int wrow = tr.r0;
-    float2 ref[kRT][NP];
-    Band band[kRT];
-    uint32_t cA[kRT], c2[kRT], c3[kRT];
-    int nev[kRT];
-    float hmax = 0.0f;
-#pragma unroll
-    for (int r = 0; r < kRT; ++r) {
-        const int idx = wrow + r * 32 + lane;
-        const bool valid = idx < ci.n;
-        load_ref<D>(ref[r], cp + (int64_t)idx * DP, valid);
-        band[r] = make_band(valid ? t32_in[ci.row0 + idx] : 0.0f, ci.delta);
-        if (!valid) {  // empty band: never inside, never an event
-            band[r].lo = -INFINITY;
-            band[r].nlo = INFINITY;
-            band[r].hi = -INFINITY;
-            band[r].w = -1.0f;
-        } else {
-            hmax = fmaxf(hmax, band[r].hi);
-        }
-        cA[r] = c2[r] = c3[r] = 0;
-        nev[r] = 0;
-    }
-    const float bound = warp_max_nonneg(hmax);
-    constexpr int NG = DY < kGate ? DY : kGate;
-    auto refs_need = [&](const Box<1> &b) {
-        bool need = !prune;
-#pragma unroll
-        for (int r = 0; r < kRT; ++r) need |= point_box<1, NG, NP, 1>(ref[r], b) <= band[r].hi;
-        return need;
-    };
-    if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
-    fence_barrier_init();
-    __syncwarp();
-    Walker<1> wk;
-    wk.init(fb, wrow, ci.n, ci.npad);
-    int slot_st = -1;
-    int issued = 0;
-    uint32_t nsub = 0;
-    for (; issued < NSLOT; ++issued) {
-        const int st = wk.next(fb, prune ? bound : INFINITY, false, refs_need);
-        if (st < 0) break;
-        if (lane == issued) slot_st = st;
-        if (lane == 0) ring_issue(ring, issued, cp + (int64_t)st * kSub * DP);
-    }
-    for (int used = 0; used < issued; ++used) {
-        const int slot = used % NSLOT;
-        const int cur_st = __shfl_sync(0xffffffffu, slot_st, slot);
-        mbar_wait(&ring.full[slot], (uint32_t)(used / NSLOT) & 1u);
-        const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[slot]);
-        constexpr int NQ = DP / 4;
-        float4 nxt[NQ];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) nxt[q] = tile[q];
-#pragma unroll 2
-        for (int j = 0; j < kSub; ++j) {
-            float4 cur[NQ];
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) cur[q] = nxt[q];
-            if (j + 1 < kSub) {  // prefetch the next candidate row
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) nxt[q] = tile[(j + 1) * NQ + q];
-            }
-            const float2 *c = reinterpret_cast<const float2 *>(cur);
-            float a[kRT][2 * NP];
-            float vA[kRT];
-            bool need[kRT];
-#pragma unroll
-            for (int r = 0; r < kRT; ++r) {
-                diff_pairs<D, 0, PG>(ref[r], c, a[r]);
-                vA[r] = maxabs0<1, 1 + DY, 2 * NP>(a[r]);
-                need[r] = vA[r] <= band[r].hi;
-            }
-            // one warp vote per reference slot: the slots hold the two halves
-            // of the warp's Morton-ordered group, so a candidate often matters
-            // to one half only
-#pragma unroll
-            for (int r = 0; r < kRT; ++r) {
-                if (!__any_sync(0xffffffffu, need[r])) continue;
-                diff_pairs<D, PG, NP>(ref[r], c, a[r]);
-                const float A = vA[r];
-                const float m2 = fmaxf(A, fabsf(a[r][0]));
-                const float m3 = maxabs<1 + DY, D, 2 * NP>(a[r], A);
-                const float jd = fmaxf(m2, m3);
-                // certain-inside counts: sign bit of (v - lo)
-                const float2 e = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nlo, band[r].nlo));
-                const float e3 = m3 + band[r].nlo;
-                cA[r] += __float_as_uint(e.x) >> 31;
-                c2[r] += __float_as_uint(e.y) >> 31;
-                c3[r] += __float_as_uint(e3) >> 31;
-                // conservative band test: min |v - t| <= w
-                const float2 b1 = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nt, band[r].nt));
-                const float2 b2 = __fadd2_rn(make_float2(m3, jd), make_float2(band[r].nt, band[r].nt));
-                const float bm = fminf(fminf(fabsf(b1.x), fabsf(b1.y)), fminf(fabsf(b2.x), fabsf(b2.y)));
-                if (bm <= band[r].w) {
-                    const float lo = band[r].lo, hi = band[r].hi;
-                    uint32_t f = ((A >= lo && A <= hi) ? 1u : 0u) | ((m2 >= lo && m2 <= hi) ? 2u : 0u) |
-                                 ((m3 >= lo && m3 <= hi) ? 4u : 0u) | ((jd >= lo && jd <= hi) ? 8u : 0u);
-                    f &= fmask;
-                    if (f) {
-                        const int idx = wrow + r * 32 + lane;
-                        const int jg = cur_st * kSub + j;
-                        if (nev[r] < kCap) ev[(ci.row0 + idx) * kCap + nev[r]] = (uint32_t)jg | (f << 28);
-                        ++nev[r];
-                    }
-                }
-            }
-        }
-        ++nsub;
-        __syncwarp();
-        const int st = wk.next(fb, prune ? bound : INFINITY, false, refs_need);
-        if (st >= 0) {
-            if (lane == issued % NSLOT) slot_st = st;
-            if (lane == 0) ring_issue(ring, issued % NSLOT, cp + (int64_t)st * kSub * DP);
-            ++issued;
-        }
-    }
-    if (lane == 0) atomicAdd(work, (unsigned long long)nsub);
-#pragma unroll
-    for (int r = 0; r < kRT; ++r) {
-        const int idx = wrow + r * 32 + lane;
-        if (idx >= ci.n) continue;
-        const uint32_t self = band[r].lo > 0.0f ? 1u : 0u;  // the self pair counted as inside
-        const int64_t row = ci.row0 + idx;
-        cnt_out[row] = (int32_t)(cA[r] - self);
-        cnt_out[ws_rows + row] = (int32_t)(c2[r] - self);
-        cnt_out[2 * ws_rows + row] = (int32_t)(c3[r] - self);
-        ev_n[row] = nev[r];
-    }
-}
-
-// ---------------------------------------------------------------------------
-// pass 2: certain counts in the three TE marginals + band events
-//   marginal 0 = y-past (A), 1 = y + y-past (m2), 2 = y-past + x-past (m3)
-//   A <= every marginal and the joint, so A > hi settles a pair (outside
-//   everywhere, no event) after the gate columns alone.
-//
-// References are compacted.  The warp's 64 references live in
-// shared memory (coordinates, band, counts, event fill); for every streamed
-// sub-tile the walker's per-reference point-to-box tests say which of them
-// can have a pair inside the band (about a third of an evaluated sub-tile's
-// references), and only those are packed onto the lanes, one per lane, in
-// rounds of 32 -- most sub-tiles need one round instead of the two a fixed
-// two-references-per-lane mapping costs.  Per round a lane reloads its
-// reference from shared memory and folds its counts back afterwards.
-// ---------------------------------------------------------------------------
-template <int DP, int NSLOT>
-struct CountRefs {
-    float ref[32 * kRT][DP];  // fp32 centred coordinates
-    float lo[32 * kRT], hi[32 * kRT], t[32 * kRT], w[32 * kRT];
-    uint32_t cnt[3][32 * kRT];
-    int nev[32 * kRT];
-    int slot[32 * kRT];       // compacted reference list of the current sub-tile
-};
-
-template <int DY, int DX>
-__global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) count_pass_kernel(
-    const float *__restrict__ pts32, const float *__restrict__ fbox,
-    const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks,
-    const float *__restrict__ t32_in, int64_t ws_rows, int prune, int32_t *__restrict__ cnt_out,
-    uint32_t *__restrict__ ev, int32_t *__restrict__ ev_n, uint32_t fmask,
-    unsigned long long *__restrict__ work) {
-    using L = Lay<DY, DX>;
-    constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG;
-    constexpr int NSLOT = L::NSLOT < ENTE_CNT_NSLOT ? L::NSLOT : ENTE_CNT_NSLOT;
-    __shared__ __align__(128) Ring<DP, NSLOT> ring;
-    __shared__ __align__(16) CountRefs<DP, NSLOT> rs;
-    const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
-    const ChunkInfo ci = info[tr.chunk];
-    if (!ci.ok32) return;
-    const int lane = threadIdx.x;
-    const unsigned lt = (1u << lane) - 1u;
-    const float *cp = pts32 + ci.prow0 * DP;
-    const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2;
-    const int wrow = tr.r0;
-    float2 myref[kRT][NP];  // this lane's own references (walker tests)
-    float myhi[kRT];
-    float hmax = 0.0f;
-#pragma unroll
-    for (int r = 0; r < kRT; ++r) {
-        const int ri = r * 32 + lane;
-        const int idx = wrow + ri;
-        const bool valid = idx < ci.n;
-        load_ref<D>(myref[r], cp + (int64_t)idx * DP, valid);
-#pragma unroll
-        for (int c = 0; c < DP; ++c) rs.ref[ri][c] = (valid && c < D) ? cp[(int64_t)idx * DP + c] : 0.0f;
-        Band b = make_band(valid ? t32_in[ci.row0 + idx] : 0.0f, ci.delta);
-        if (!valid) {  // empty band: never inside, never an event, never needed
-            b.lo = -INFINITY;
-            b.hi = -INFINITY;
-            b.w = -1.0f;
-            b.nt = 0.0f;
-        } else {
-            hmax = fmaxf(hmax, b.hi);
-        }
-        rs.lo[ri] = b.lo;
-        rs.hi[ri] = b.hi;
-        rs.t[ri] = b.nt;
-        rs.w[ri] = b.w;
-        myhi[r] = b.hi;
-        rs.cnt[0][ri] = rs.cnt[1][ri] = rs.cnt[2][ri] = 0u;
-        rs.nev[ri] = 0;
-    }
-    const float bound = warp_max_nonneg(hmax);
-    constexpr int NG = DY < kGate ? DY : kGate;
-    auto refs_need = [&](const Box<1> &b) {
-        uint32_t need = 0u;
-#pragma unroll
-        for (int r = 0; r < kRT; ++r)
-            need |= ((!prune && myhi[r] > -INFINITY) || point_box<1, NG, NP, 1>(myref[r], b) <= myhi[r])
-                        ? (1u << r) : 0u;
-        return need;
-    };
-    if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
-    fence_barrier_init();
-    __syncwarp();
-    Walker<1> wk;
-    wk.init(fb, wrow, ci.n, ci.npad);
-    int slot_st = -1;
-    uint32_t slot_need = 0u;  // kRT bits per ring slot: this lane's needs of the issued sub-tiles
-    int issued = 0;
-    uint32_t nsub = 0;
-    for (; issued < NSLOT; ++issued) {
-        const int st = wk.next(fb, prune ? bound : INFINITY, false, refs_need);
-        if (st < 0) break;
-        if (lane == issued) slot_st = st;
-        slot_need |= wk.need << (kRT * issued);
-        if (lane == 0) ring_issue(ring, issued, cp + (int64_t)st * kSub * DP);
-    }
-    for (int used = 0; used < issued; ++used) {
-        const int slot = used % NSLOT;
-        const int cur_st = __shfl_sync(0xffffffffu, slot_st, slot);
-        const uint32_t nb = (slot_need >> (kRT * slot)) & ((1u << kRT) - 1u);
-        // compact the references that need this sub-tile
-        int base = 0;
-#pragma unroll
-        for (int r = 0; r < kRT; ++r) {
-            const uint32_t m = __ballot_sync(0xffffffffu, (nb >> r) & 1u);
-            if ((nb >> r) & 1u) rs.slot[base + __popc(m & lt)] = r * 32 + lane;
-            base += __popc(m);
-        }
-        const int nneed = base;
-        __syncwarp();
-        mbar_wait(&ring.full[slot], (uint32_t)(used / NSLOT) & 1u);
-        const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[slot]);
-        constexpr int NQ = DP / 4;
-        for (int round = 0; round < nneed; round += 32) {
-            const bool active = round + lane < nneed;
-            const int ri = active ? rs.slot[round + lane] : 0;
-            float2 ref[NP];
-            {
-                const float2 *rr = reinterpret_cast<const float2 *>(rs.ref[ri]);
-#pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    const float2 v = rr[p];
-                    ref[p] = make_float2(-v.x, -v.y);
-                }
-            }
-            const float lo = active ? rs.lo[ri] : -INFINITY;
-            const float hi = active ? rs.hi[ri] : -INFINITY;
-            const float nlo = -lo, nt = rs.t[ri], wb = active ? rs.w[ri] : -1.0f;
-            uint32_t cA = 0u, c2 = 0u, c3 = 0u;
-            int nev = active ? rs.nev[ri] : 0;
-            const int64_t evrow = (ci.row0 + wrow + ri) * kCap;
-            // one candidate row against this lane's reference
-            auto visit = [&](const float4 (&cur)[NQ], int j) {
-                const float2 *c = reinterpret_cast<const float2 *>(cur);
-                float a[2 * NP];
-                diff_pairs<D, 0, PG>(ref, c, a);
-                const float A = maxabs0<1, 1 + DY, 2 * NP>(a);
-                if (!__any_sync(0xffffffffu, A <= hi)) return;
-                diff_pairs<D, PG, NP>(ref, c, a);
-                const float m2 = fmaxf(A, fabsf(a[0]));
-                const float m3 = maxabs<1 + DY, D, 2 * NP>(a, A);
-                const float jd = fmaxf(m2, m3);
-                const float2 e = __fadd2_rn(make_float2(A, m2), make_float2(nlo, nlo));
-                const float e3 = m3 + nlo;
-                cA += __float_as_uint(e.x) >> 31;
-                c2 += __float_as_uint(e.y) >> 31;
-                c3 += __float_as_uint(e3) >> 31;
-                const float2 b1 = __fadd2_rn(make_float2(A, m2), make_float2(nt, nt));
-                const float2 b2 = __fadd2_rn(make_float2(m3, jd), make_float2(nt, nt));
-                const float bm = fminf(fminf(fabsf(b1.x), fabsf(b1.y)), fminf(fabsf(b2.x), fabsf(b2.y)));
-                if (bm <= wb) {
-                    uint32_t f = ((A >= lo && A <= hi) ? 1u : 0u) | ((m2 >= lo && m2 <= hi) ? 2u : 0u) |
-                                 ((m3 >= lo && m3 <= hi) ? 4u : 0u) | ((jd >= lo && jd <= hi) ? 8u : 0u);
-                    f &= fmask;
-                    if (f) {
-                        if (nev < kCap) ev[evrow + nev] = (uint32_t)(cur_st * kSub + j) | (f << 28);
-                        ++nev;
-                    }
-                }
-            };
-            // ping-pong row registers: the next row's LDS overlaps this row's math
-            float4 ra[NQ], rb[NQ];
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) ra[q] = tile[q];
-            for (int j = 0; j < kSub; j += 2) {
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) rb[q] = tile[(j + 1) * NQ + q];
-                visit(ra, j);
-                if (j + 2 < kSub) {
-#pragma unroll
-                    for (int q = 0; q < NQ; ++q) ra[q] = tile[(j + 2) * NQ + q];
-                }
-                visit(rb, j + 1);
-            }
-            if (active) {
-                rs.cnt[0][ri] += cA;
-                rs.cnt[1][ri] += c2;
-                rs.cnt[2][ri] += c3;
-                rs.nev[ri] = nev;
-            }
-            __syncwarp();
-        }
-        ++nsub;
-        __syncwarp();
-        const int st = wk.next(fb, prune ? bound : INFINITY, false, refs_need);
-        if (st >= 0) {
-            const int ns = issued % NSLOT;
-            if (lane == ns) slot_st = st;
-            slot_need = (slot_need & ~(((1u << kRT) - 1u) << (kRT * ns))) | (wk.need << (kRT * ns));
-            if (lane == 0) ring_issue(ring, ns, cp + (int64_t)st * kSub * DP);
-            ++issued;
-        }
-    }
-    if (lane == 0) atomicAdd(work, (unsigned long long)nsub);
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < kRT; ++r) {
-        const int ri = r * 32 + lane;
-        const int idx = wrow + ri;
-        if (idx >= ci.n) continue;
-        const uint32_t self = rs.lo[ri] > 0.0f ? 1u : 0u;  // the self pair counted as inside
-        const int64_t row = ci.row0 + idx;
-        cnt_out[row] = (int32_t)(rs.cnt[0][ri] - self);
-        cnt_out[ws_rows + row] = (int32_t)(rs.cnt[1][ri] - self);
-        cnt_out[2 * ws_rows + row] = (int32_t)(rs.cnt[2][ri] - self);
-        ev_n[row] = rs.nev[ri];
-    }
-}
-
-// ---------------------------------------------------------------------------
-// resolve: fp64 certification of band events (sorted positions -> rows via perm)
-// one thread per reference of a 128-reference tile
-// ---------------------------------------------------------------------------
-struct TeLayout {
-    int dy;
-    int nout;
-    int slot[kMaxMarg];  // output o <- TE marginal slot (0, 1, 2)
-};
-
-__device__ __forceinline__ void te_dist64(const double *ref, const double *q, int dim, int dy,
-                                          double &A, double &m2, double &m3, double &jd) {
-    double a = 0.0, b = 0.0;
-    for (int c = 1; c < dim; ++c) {
-        const double v = fabs(__dsub_rn(ref[c], q[c]));
-        if (c <= dy) a = fmax(a, v);
-        else b = fmax(b, v);
-    }
-    const double y = fabs(__dsub_rn(ref[0], q[0]));
-    A = a;
-    m2 = fmax(a, y);
-    m3 = fmax(a, b);
-    jd = fmax(m2, m3);
-}
-
 __global__ void __launch_bounds__(kWarpRefs) resolve_kernel(
     const double *__restrict__ pts64, int dim, const ChunkInfo *__restrict__ info,
     const int32_t *__restrict__ tile0, int n_chunks, int k, TeLayout lay, const int32_t *__restrict__ perm,
@@ -1394,152 +586,6 @@ __global__ void __launch_bounds__(kWarpRefs) resolve_kernel(
     }
 }
 
-
-// ---------------------------------------------------------------------------
-// rescan: exact eps and counts for references whose band events overflowed
-// (heavily tied data).  One warp per listed sorted row; the lanes take the
-// 32 candidates of a sub-tile, sub-tiles are pruned by their gate boxes, and
-// every candidate the fp32 filter cannot decide is settled in fp64 on the
-// spot, so there is no per-point event limit:
-//   A  eps = k-th smallest joint d64 over the candidates with d32 <= hiA,
-//      hiA = up(t32 + 2 delta) (they include the true k nearest); per-lane
-//      sorted fp64 lists, k rounds of warp-minimum extraction
-//   B  with eps exact: v32 < lo = down(eps - delta) -> inside,
-//      v32 > hi = up(eps + delta) -> outside, otherwise compare v64 < eps
-// ---------------------------------------------------------------------------
-constexpr int kRescanWarps = 4;
-
-template <int DY, int DX, int S>
-__global__ void __launch_bounds__(kRescanWarps * 32) rescan_kernel(
-    const float *__restrict__ pts32, const float *__restrict__ fbox, const double *__restrict__ pts64,
-    const ChunkInfo *__restrict__ info, int n_chunks, const int32_t *__restrict__ perm,
-    const float *__restrict__ t32_in, const int64_t *__restrict__ list,
-    const int32_t *__restrict__ list_n, int k, TeLayout lay, int64_t total_rows,
-    double *__restrict__ out_eps, int32_t *__restrict__ out_counts) {
-    using L = Lay<DY, DX>;
-    constexpr int D = L::D, DP = L::DP, NP = L::NP;
-    constexpr int NG = DY < kGate ? DY : kGate;
-    const int lane = threadIdx.x & 31;
-    const int64_t nwarps = (int64_t)gridDim.x * kRescanWarps;
-    const int64_t count = *list_n;
-    for (int64_t it = (int64_t)blockIdx.x * kRescanWarps + (threadIdx.x >> 5); it < count;
-         it += nwarps) {
-        const int64_t srow = list[it];
-        const int c = chunk_of_row(info, n_chunks, srow);
-        const ChunkInfo ci = info[c];
-        const int s = (int)(srow - ci.row0);  // sorted position of the reference
-        const int64_t row = ci.row0 + perm[srow];
-        const float *cp = pts32 + ci.prow0 * DP;
-        const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2;
-        const int nsub = ci.npad / kSub;
-        float2 ref[NP];
-        load_ref<D>(ref, cp + (int64_t)s * DP, true);
-        double r64[D];
-#pragma unroll
-        for (int col = 0; col < D; ++col) r64[col] = pts64[row * D + col];
-        const double delta = ci.delta;
-        const float hiA = __double2float_ru(__dadd_ru((double)t32_in[srow], 2.0 * delta));
-        // ---- phase A: exact k-th joint distance
-        double kd[S];
-#pragma unroll
-        for (int q = 0; q < S; ++q) kd[q] = (q < S - k) ? -INFINITY : INFINITY;
-        for (int base = 0; base < nsub; base += 32) {
-            const int st_l = base + lane;
-            bool need = false;
-            if (st_l < nsub) need = point_box<1, NG, NP, 1>(ref, load_box<1>(fb, st_l)) <= hiA;
-            uint32_t m = __ballot_sync(0xffffffffu, need);
-            while (m) {
-                const int st = base + __ffs(m) - 1;
-                m &= m - 1;
-                const int j = st * kSub + lane;
-                const float *q = cp + (int64_t)(lane < kSub ? j : st * kSub) * DP;
-                float d = 0.0f;
-#pragma unroll
-                for (int col = 0; col < D; ++col) {
-                    const float x = (col & 1) ? ref[col >> 1].y : ref[col >> 1].x;
-                    d = fmaxf(d, fabsf(q[col] + x));
-                }
-                if (lane < kSub && j < ci.n && j != s && d <= hiA) {
-                    const double *q64 = pts64 + (ci.row0 + perm[ci.row0 + j]) * D;
-                    double d64 = 0.0;
-#pragma unroll
-                    for (int col = 0; col < D; ++col) d64 = fmax(d64, fabs(__dsub_rn(r64[col], q64[col])));
-                    if (d64 < kd[S - 1]) {
-#pragma unroll
-                        for (int q2 = S - 1; q2 >= 1; --q2) kd[q2] = fmax(kd[q2 - 1], fmin(kd[q2], d64));
-                        kd[0] = fmin(kd[0], d64);
-                    }
-                }
-            }
-        }
-        double eps = 0.0;
-        for (int q = 0; q < k; ++q) {
-            const double v = kd[S - k];
-            double mn = v;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-            const unsigned win = __ffs(__ballot_sync(0xffffffffu, v == mn)) - 1;
-            if ((unsigned)lane == win) {
-#pragma unroll
-                for (int q2 = 0; q2 < S - 1; ++q2)
-                    if (q2 >= S - k) kd[q2] = kd[q2 + 1];
-                kd[S - 1] = INFINITY;
-            }
-            eps = mn;
-        }
-        // ---- phase B: strict counts in the three TE marginals
-        const float lo = __double2float_rd(__dsub_rd(eps, delta));
-        const float hi = __double2float_ru(__dadd_ru(eps, delta));
-        int cnt[3] = {0, 0, 0};
-        for (int base = 0; base < nsub; base += 32) {
-            const int st_l = base + lane;
-            bool need = false;
-            if (st_l < nsub) need = point_box<1, NG, NP, 1>(ref, load_box<1>(fb, st_l)) <= hi;
-            uint32_t m = __ballot_sync(0xffffffffu, need);
-            while (m) {
-                const int st = base + __ffs(m) - 1;
-                m &= m - 1;
-                const int j = st * kSub + lane;
-                if (lane >= kSub || j >= ci.n || j == s) continue;
-                const float *q = cp + (int64_t)j * DP;
-                float a = 0.0f, b = 0.0f;
-#pragma unroll
-                for (int col = 1; col < D; ++col) {
-                    const float x = (col & 1) ? ref[col >> 1].y : ref[col >> 1].x;
-                    const float v = fabsf(q[col] + x);
-                    if (col <= DY) a = fmaxf(a, v);
-                    else b = fmaxf(b, v);
-                }
-                const float y = fabsf(q[0] + ref[0].x);
-                const float v32[3] = {a, fmaxf(a, y), fmaxf(a, b)};
-                bool amb = false;
-#pragma unroll
-                for (int o = 0; o < 3; ++o) {
-                    cnt[o] += v32[o] < lo;
-                    amb |= (v32[o] >= lo && v32[o] <= hi);
-                }
-                if (amb) {
-                    double A, m2, m3, jd;
-                    te_dist64(r64, pts64 + (ci.row0 + perm[ci.row0 + j]) * D, D, DY, A, m2, m3, jd);
-                    const double v64[3] = {A, m2, m3};
-#pragma unroll
-                    for (int o = 0; o < 3; ++o)
-                        cnt[o] += (v32[o] >= lo && v32[o] <= hi) && (v64[o] < eps);
-                }
-            }
-        }
-#pragma unroll
-        for (int o = 0; o < 3; ++o) {
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) cnt[o] += __shfl_xor_sync(0xffffffffu, cnt[o], off);
-        }
-        if (lane == 0) {
-            out_eps[row] = eps;
-            for (int o = 0; o < lay.nout; ++o) out_counts[o * total_rows + row] = cnt[lay.slot[o]];
-        }
-        __syncwarp();
-    }
-}
 // ---------------------------------------------------------------------------
 // exact: one warp per point, fp64 scan, warp-shuffle top-k merge
 // ---------------------------------------------------------------------------
@@ -1764,51 +810,18 @@ __global__ void __launch_bounds__(kIdxWarps * 32) knn_index_kernel(
 // ---------------------------------------------------------------------------
 // host side: kernel tables and dispatch
 // ---------------------------------------------------------------------------
-using KnnFn = void (*)(const float *, const float *, const ChunkInfo *, const int32_t *, int, int,
-                       int, const int32_t *, float *, int32_t *, unsigned long long *);
-using CountFn = void (*)(const float *, const float *, const ChunkInfo *, const int32_t *, int,
-                         const float *, int64_t, int, int32_t *, uint32_t *, int32_t *, uint32_t,
-                         unsigned long long *);
-
-// (DY, DX) layouts with compiled sweeps: TE embeddings d_y, d_x <= 3, the
-// symmetric C3 sweep (1+2d) and the bench layout (marginal = first m cols).
-#define ENTE_TE_LAYOUTS(X)                                                                  \
-    X(1, 1) X(1, 2) X(2, 1) X(2, 2) X(1, 3) X(3, 1) X(2, 3) X(3, 2) X(3, 3) X(4, 4) X(5, 5) \
-    X(6, 6) X(7, 7) X(8, 8) X(0, 2) X(1, 4) X(2, 4) X(3, 5) X(4, 6) X(5, 7) X(6, 8) X(7, 9)
-
-template <int DY, int DX>
-static KnnFn knn_for_slots(int slots) {
-    if (slots <= 5) return knn_pass_kernel<DY, DX, 5>;
-    if (slots <= 8) return knn_pass_kernel<DY, DX, 8>;
-    if (slots <= 16) return knn_pass_kernel<DY, DX, 16>;
-    return nullptr;
-}
-
+// Layout tables: the sweeps of every compiled (d_y, d_x) live in the
+// sweeps_*.cu translation units (sweeps.cuh).
 static KnnFn knn_table(int dy, int dx, int slots) {
-#define ENTE_CASE(a, b) \
-    if (dy == a && dx == b) return knn_for_slots<a, b>(slots);
-    ENTE_TE_LAYOUTS(ENTE_CASE)
-#undef ENTE_CASE
-    return nullptr;
-}
-
-using RescanFn = void (*)(const float *, const float *, const double *, const ChunkInfo *, int,
-                          const int32_t *, const float *, const int64_t *, const int32_t *, int,
-                          TeLayout, int64_t, double *, int32_t *);
-
-template <int DY, int DX>
-static RescanFn rescan_for_k(int k) {
-    if (k <= 4) return rescan_kernel<DY, DX, 4>;
-    if (k <= 8) return rescan_kernel<DY, DX, 8>;
-    return rescan_kernel<DY, DX, 16>;
+    SweepSet ss;
+    if (!find_sweep_set(dy, dx, ss)) return nullptr;
+    return slots <= 5 ? ss.knn[0] : slots <= 8 ? ss.knn[1] : slots <= 16 ? ss.knn[2] : nullptr;
 }
 
 static RescanFn rescan_table(int dy, int dx, int k) {
-#define ENTE_CASE(a, b) \
-    if (dy == a && dx == b) return rescan_for_k<a, b>(k);
-    ENTE_TE_LAYOUTS(ENTE_CASE)
-#undef ENTE_CASE
-    return nullptr;
+    SweepSet ss;
+    if (!find_sweep_set(dy, dx, ss)) return nullptr;
+    return k <= 4 ? ss.rescan[0] : k <= 8 ? ss.rescan[1] : ss.rescan[2];
 }
 
 // Chunks of a few sub-tiles: nearly every reference needs every sub-tile,
@@ -1816,12 +829,9 @@ static RescanFn rescan_table(int dy, int dx, int k) {
 constexpr int kCompactMinRows = 4096;
 
 static CountFn count_table(int dy, int dx, int max_npad) {
-#define ENTE_CASE(a, b) \
-    if (dy == a && dx == b) \
-        return max_npad >= kCompactMinRows ? count_pass_kernel<a, b> : count_pass_direct_kernel<a, b>;
-    ENTE_TE_LAYOUTS(ENTE_CASE)
-#undef ENTE_CASE
-    return nullptr;
+    SweepSet ss;
+    if (!find_sweep_set(dy, dx, ss)) return nullptr;
+    return max_npad >= kCompactMinRows ? ss.compact : ss.direct;
 }
 
 struct Plan {
@@ -1840,8 +850,19 @@ static bool match_te_layout(int dim, const uint32_t *masks, int n_marg, int &dy_
                             TeLayout &lay) {
     const uint32_t all_but_0 = ((dim >= 32) ? 0xFFFFFFFFu : ((1u << dim) - 1u)) & ~1u;
     // with no marginals any layout of the right width serves (the gate is then
-    // only a lower bound of the joint distance): prefer a y-past block
-    for (int dy = n_marg == 0 ? 1 : 0; dy < dim; ++dy) {
+    // only a lower bound of the joint distance): prefer a 3-column gate block
+    // (the Morton key and the gate boxes use up to kGate columns)
+    int order[kMaxDim];
+    int no = 0;
+    if (n_marg == 0) {
+        const int pref = dim - 1 < 3 ? dim - 1 : 3;
+        for (int d = pref; d >= 1; --d) order[no++] = d;
+        for (int d = pref + 1; d < dim; ++d) order[no++] = d;
+    } else {
+        for (int d = 0; d < dim; ++d) order[no++] = d;
+    }
+    for (int oi = 0; oi < no; ++oi) {
+        const int dy = order[oi];
         const uint32_t yp = ((1u << (dy + 1)) - 1u) & ~1u;  // cols 1..dy
         const uint32_t yyp = (1u << (dy + 1)) - 1u;         // cols 0..dy
         bool ok = true;
