@@ -815,13 +815,15 @@ __global__ void __launch_bounds__(kIdxWarps * 32) knn_index_kernel(
 static KnnFn knn_table(int dy, int dx, int slots) {
     SweepSet ss;
     if (!find_sweep_set(dy, dx, ss)) return nullptr;
-    return slots <= 5 ? ss.knn[0] : slots <= 8 ? ss.knn[1] : slots <= 16 ? ss.knn[2] : nullptr;
+    return slots <= 5 ? ss.knn[0] : slots <= 8 ? ss.knn[1] : slots <= 16 ? ss.knn[2]
+         : slots <= 32 ? ss.knn[3] : slots <= 64 ? ss.knn[4] : nullptr;
 }
 
 static RescanFn rescan_table(int dy, int dx, int k) {
     SweepSet ss;
     if (!find_sweep_set(dy, dx, ss)) return nullptr;
-    return k <= 4 ? ss.rescan[0] : k <= 8 ? ss.rescan[1] : ss.rescan[2];
+    return k <= 4 ? ss.rescan[0] : k <= 8 ? ss.rescan[1] : k <= 16 ? ss.rescan[2]
+         : k <= 32 ? ss.rescan[3] : ss.rescan[4];
 }
 
 // Chunks of a few sub-tiles: nearly every reference needs every sub-tile,
@@ -914,7 +916,7 @@ static Plan make_plan(const ente_chunk *chunks, int n_chunks, int dim, const uin
     }
     int dy = 0;
     TeLayout lay{};
-    if (k + 1 <= 16 && match_te_layout(dim, masks, n_marg, dy, lay) &&
+    if (k + 1 <= 64 && match_te_layout(dim, masks, n_marg, dy, lay) &&
         knn_table(dy, dim - 1 - dy, k + 1)) {
         p.fast = true;
         p.dy = dy;
@@ -1144,7 +1146,7 @@ extern "C" size_t ente_search_workspace_size(const ente_chunk *chunks, int n_chu
     uint32_t dummy[kMaxMarg] = {0};
     Plan p = make_plan(chunks, n_chunks, dim, dummy, 0, k);
     // size for the fast path whenever it could be taken
-    if (k + 1 <= 16) {
+    if (k + 1 <= 64) {
         p.fast = true;
         p.dp = (dim + 3) & ~3;
     }

@@ -314,7 +314,7 @@ __device__ __forceinline__ void ring_issue(Ring<DP, NSLOT> &ring, int slot, cons
 // lane l owns sorted rows wrow + r*32 + l, r < kRT
 // ---------------------------------------------------------------------------
 template <int DY, int DX, int S>
-__global__ void __launch_bounds__(32, S > 8 ? 16 : sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) knn_pass_kernel(
+__global__ void __launch_bounds__(32, S > 16 ? 24 : (S > 8 ? 16 : sweep_minb(1 + DY + DX, ENTE_KNN_MINB))) knn_pass_kernel(
     const float *__restrict__ pts32, const float *__restrict__ fbox,
     const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks, int k, int prune,
     const int32_t *__restrict__ kmap, float *__restrict__ t32_out, int32_t *__restrict__ L_out,
@@ -324,6 +324,11 @@ __global__ void __launch_bounds__(32, S > 8 ? 16 : sweep_minb(1 + DY + DX, ENTE_
     constexpr int NSLOT = L::NSLOT < ENTE_KNN_NSLOT ? L::NSLOT : ENTE_KNN_NSLOT;
     constexpr int NBC = D < 4 * kKnnQ ? D : 4 * kKnnQ;  // box columns 0 .. NBC-1
     __shared__ __align__(128) Ring<DP, NSLOT> ring;
+    // k + 1 > 16 slots: the sorted lists live in shared memory ([ref][slot][lane],
+    // conflict-free), only their last entry (the current k-th) in a register
+    constexpr bool SL = S > 16;
+    constexpr int SR = SL ? 1 : S;
+    __shared__ float lst[SL ? kRT : 1][SL ? S : 1][32];
     const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
@@ -332,15 +337,34 @@ __global__ void __launch_bounds__(32, S > 8 ? 16 : sweep_minb(1 + DY + DX, ENTE_
     const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2 * kKnnQ;
     const int wrow = tr.r0;
     float2 ref[kRT][NP];
-    float kd[kRT][S];
+    float kd[kRT][SR];  // register list, or (SL) the current k-th only
 #pragma unroll
     for (int r = 0; r < kRT; ++r) {
         const int idx = wrow + r * 32 + lane;
         const bool valid = idx < ci.n;
         load_ref<D>(ref[r], cp + (int64_t)idx * DP, valid);
+        if constexpr (SL) {
+            for (int s = 0; s < S; ++s) lst[r][s][lane] = (!valid || s < S - (k + 1)) ? -INFINITY : INFINITY;
+            kd[r][0] = valid ? INFINITY : -INFINITY;
+        } else {
 #pragma unroll
-        for (int s = 0; s < S; ++s) kd[r][s] = (!valid || s < S - (k + 1)) ? -INFINITY : INFINITY;
+            for (int s = 0; s < S; ++s) kd[r][s] = (!valid || s < S - (k + 1)) ? -INFINITY : INFINITY;
+        }
     }
+    // sorted insertion of d < current k-th into reference slot r's list
+    auto insert = [&](int r, float d) {
+        if constexpr (SL) {
+            int p = S - 1;
+            while (p > 0 && lst[r][p - 1][lane] > d) {
+                lst[r][p][lane] = lst[r][p - 1][lane];
+                --p;
+            }
+            lst[r][p][lane] = d;
+            kd[r][0] = lst[r][S - 1][lane];
+        } else {
+            insert_sorted<S>(kd[r], d);
+        }
+    };
     if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
     fence_barrier_init();
     __syncwarp();
@@ -350,7 +374,7 @@ __global__ void __launch_bounds__(32, S > 8 ? 16 : sweep_minb(1 + DY + DX, ENTE_
     auto refs_need = [&](const Box<kKnnQ> &b) {
         bool need = !prune;
 #pragma unroll
-        for (int r = 0; r < kRT; ++r) need |= point_box<0, NBC, NP, kKnnQ>(ref[r], b) < kd[r][S - 1];
+        for (int r = 0; r < kRT; ++r) need |= point_box<0, NBC, NP, kKnnQ>(ref[r], b) < kd[r][SR - 1];
         return need;
     };
     int slot_st = -1;        // lane s: sub-tile in ring slot s
@@ -388,7 +412,7 @@ __global__ void __launch_bounds__(32, S > 8 ? 16 : sweep_minb(1 + DY + DX, ENTE_
             for (int r = 0; r < kRT; ++r) {
                 diff_pairs<D, 0, PG>(ref[r], c, a[r]);
                 dj[r] = maxabs0<0, G, 2 * NP>(a[r]);
-                need |= dj[r] < kd[r][S - 1];
+                need |= dj[r] < kd[r][SR - 1];
             }
             if (__any_sync(0xffffffffu, need)) {
                 bool ins = false;
@@ -396,18 +420,19 @@ __global__ void __launch_bounds__(32, S > 8 ? 16 : sweep_minb(1 + DY + DX, ENTE_
                 for (int r = 0; r < kRT; ++r) {
                     diff_pairs<D, PG, NP>(ref[r], c, a[r]);
                     dj[r] = maxabs<G, D, 2 * NP>(a[r], dj[r]);
-                    ins |= dj[r] < kd[r][S - 1];
+                    ins |= dj[r] < kd[r][SR - 1];
                 }
                 if (ins) {
 #pragma unroll
-                    for (int r = 0; r < kRT; ++r) insert_sorted<S>(kd[r], dj[r]);
+                    for (int r = 0; r < kRT; ++r)
+                        if (SL ? dj[r] < kd[r][0] : true) insert(r, dj[r]);
                 }
             }
         }
         ++nsub;
         float wb = 0.0f;
 #pragma unroll
-        for (int r = 0; r < kRT; ++r) wb = fmaxf(wb, kd[r][S - 1]);
+        for (int r = 0; r < kRT; ++r) wb = fmaxf(wb, kd[r][SR - 1]);
         bound = warp_max_nonneg(wb);
         __syncwarp();
         const int st = wk.next(fb, prune ? bound : INFINITY, true, refs_need);
@@ -423,11 +448,15 @@ __global__ void __launch_bounds__(32, S > 8 ? 16 : sweep_minb(1 + DY + DX, ENTE_
     for (int r = 0; r < kRT; ++r) {
         const int idx = wrow + r * 32 + lane;
         if (idx >= ci.n) continue;
-        const float t32 = kd[r][S - 1];
+        const float t32 = kd[r][SR - 1];
         const float lo = __double2float_rd(__dsub_rd((double)t32, 2.0 * ci.delta));
         int Lc = 0;
+        if constexpr (SL) {
+            for (int s = 0; s < S; ++s) Lc += (lst[r][s][lane] > -INFINITY) && (lst[r][s][lane] < lo);
+        } else {
 #pragma unroll
-        for (int s = 0; s < S; ++s) Lc += (kd[r][s] > -INFINITY) && (kd[r][s] < lo);
+            for (int s = 0; s < S; ++s) Lc += (kd[r][s] > -INFINITY) && (kd[r][s] < lo);
+        }
         if (lo > 0.0f) Lc -= 1;  // the self pair (distance 0) was counted
         const int64_t orow = ci.row0 + (kmap ? kmap[ci.row0 + idx] : idx);  // count-order row
         t32_out[orow] = t32;
@@ -983,10 +1012,10 @@ using RescanFn = void (*)(const float *, const float *, const double *, const Ch
 
 // Every kernel of one compiled (d_y, d_x) TE layout.
 struct SweepSet {
-    KnnFn knn[3];      // k + 1 <= 5, 8, 16 register slots
+    KnnFn knn[5];      // k + 1 <= 5, 8, 16 register slots; 32, 64 shared-memory slots
     CountFn compact;   // count pass, compacted references (chunks >= 4096 rows)
     CountFn direct;    // count pass, two references per lane (small chunks)
-    RescanFn rescan[3];  // k <= 4, 8, 16
+    RescanFn rescan[5];  // k <= 4, 8, 16, 32, 64
 };
 
 template <int DY, int DX>
@@ -995,20 +1024,25 @@ SweepSet make_sweep_set() {
     s.knn[0] = knn_pass_kernel<DY, DX, 5>;
     s.knn[1] = knn_pass_kernel<DY, DX, 8>;
     s.knn[2] = knn_pass_kernel<DY, DX, 16>;
+    s.knn[3] = knn_pass_kernel<DY, DX, 32>;
+    s.knn[4] = knn_pass_kernel<DY, DX, 64>;
     s.compact = count_pass_kernel<DY, DX>;
     s.direct = count_pass_direct_kernel<DY, DX>;
     s.rescan[0] = rescan_kernel<DY, DX, 4>;
     s.rescan[1] = rescan_kernel<DY, DX, 8>;
     s.rescan[2] = rescan_kernel<DY, DX, 16>;
+    s.rescan[3] = rescan_kernel<DY, DX, 32>;
+    s.rescan[4] = rescan_kernel<DY, DX, 64>;
     return s;
 }
 
-// the layout groups (sweeps_a.cu, sweeps_b.cu); false when (dy, dx) is not in the group
+// the layout groups (sweeps_a/b/c.cu); false when (dy, dx) is not in the group
 bool sweep_set_a(int dy, int dx, SweepSet &out);
 bool sweep_set_b(int dy, int dx, SweepSet &out);
+bool sweep_set_c(int dy, int dx, SweepSet &out);
 
 inline bool find_sweep_set(int dy, int dx, SweepSet &out) {
-    return sweep_set_a(dy, dx, out) || sweep_set_b(dy, dx, out);
+    return sweep_set_a(dy, dx, out) || sweep_set_b(dy, dx, out) || sweep_set_c(dy, dx, out);
 }
 
 }  // namespace ente

@@ -282,3 +282,17 @@ def test_batch_search_split_single_rank_group():
         assert all(np.array_equal(a, b) for a, b in zip(r.radius_counts, c))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("k", [16, 31, 32, 47, 63])
+def test_large_k_shared_memory_lists(k):
+    """k + 1 > 16: the kNN pass keeps its sorted lists in shared memory; exact anyway."""
+    rng = np.random.default_rng(k)
+    for pts in (rng.standard_normal((4500, 7)), np.round(rng.standard_normal((3000, 5)), 1)):
+        dim = pts.shape[1]
+        dy = 3 if dim == 7 else 2
+        margs = [list(range(1, 1 + dy)), list(range(0, 1 + dy)), list(range(1, dim))]
+        (r,) = batch_search([(Chunk(pts), margs)], k)
+        e, c = oracle.search(pts, margs, k)
+        assert np.array_equal(r.kth_distance, e)
+        assert all(np.array_equal(a, b) for a, b in zip(r.radius_counts, c))
