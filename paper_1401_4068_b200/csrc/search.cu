@@ -514,6 +514,25 @@ __global__ void __launch_bounds__(kTJ) gather_kernel(const double *__restrict__ 
     }
 }
 
+// fp64 rows in the count order for chunks that have tie rescans (rs_flag):
+// the rescan then reads candidate rows of a sub-tile as one coalesced block
+// instead of one scattered row per lane
+__global__ void __launch_bounds__(kTJ) gather64_kernel(const double *__restrict__ pts64, int dim,
+                                                       const ChunkInfo *__restrict__ info, int n_chunks,
+                                                       const int32_t *__restrict__ perm,
+                                                       const int32_t *__restrict__ rs_flag,
+                                                       double *__restrict__ pts64s) {
+    for (int cidx = blockIdx.y; cidx < n_chunks; cidx += gridDim.y) {
+        if (!rs_flag[cidx]) continue;
+        const ChunkInfo ci = info[cidx];
+        const int s = blockIdx.x * kTJ + threadIdx.x;
+        if (s >= ci.n) continue;
+        const double *src = pts64 + (ci.row0 + perm[ci.row0 + s]) * dim;
+        double *dst = pts64s + (ci.prow0 + s) * dim;
+        for (int c = 0; c < dim; ++c) dst[c] = src[c];
+    }
+}
+
 __global__ void __launch_bounds__(kWarpRefs) resolve_kernel(
     const double *__restrict__ pts64, int dim, const ChunkInfo *__restrict__ info,
     const int32_t *__restrict__ tile0, int n_chunks, int k, TeLayout lay, const int32_t *__restrict__ perm,
@@ -521,7 +540,7 @@ __global__ void __launch_bounds__(kWarpRefs) resolve_kernel(
     const uint32_t *__restrict__ ev, const int32_t *__restrict__ ev_n, int64_t ws_rows,
     int64_t total_rows, double *__restrict__ out_eps, int32_t *__restrict__ out_counts,
     int64_t *__restrict__ ovf_list, int32_t *__restrict__ ovf_n, int64_t *__restrict__ rs_list,
-    int32_t *__restrict__ rs_n) {
+    int32_t *__restrict__ rs_n, int32_t *__restrict__ rs_flag) {
     const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     const int s = tr.r0 + threadIdx.x;  // sorted position
@@ -573,6 +592,7 @@ __global__ void __launch_bounds__(kWarpRefs) resolve_kernel(
         if (ci.ok32) {  // fp32 data usable: pruned warp rescan of the sorted row
             const int slot = atomicAdd(rs_n, 1);
             rs_list[slot] = srow;
+            rs_flag[tr.chunk] = 1;
         } else {
             const int slot = atomicAdd(ovf_n, 1);
             ovf_list[slot] = row;
@@ -947,6 +967,8 @@ struct SearchWs {
     int32_t *ovf_n;
     int64_t *rs;
     int32_t *rs_n;
+    int32_t *rs_flag;  // chunks with rescans
+    double *pts64s;    // their fp64 rows in the count order
     // kNN order (principal-axis Morton)
     int32_t *permk, *kmap, *inv;
     float *pts32k, *fboxk;
@@ -974,6 +996,8 @@ static SearchWs layout_ws(Arena &a, const Plan &p, int n_chunks) {
         w.ev_n = a.take<int32_t>(p.total_rows);
         w.ovf = a.take<int64_t>(p.total_rows);
         w.rs = a.take<int64_t>(p.total_rows);
+        w.rs_flag = a.take<int32_t>(n_chunks);
+        w.pts64s = a.take<double>((size_t)p.total_prows * p.dp);
         w.permk = a.take<int32_t>(p.total_rows);
         w.kmap = a.take<int32_t>(p.total_rows);
         w.inv = a.take<int32_t>(p.total_rows);
@@ -1133,6 +1157,7 @@ static int upload_chunks(cudaStream_t st, const ente_chunk *chunks, int n_chunks
     ENTE_CUDA(cudaMemcpyAsync(status, hstatus.data(), sizeof(int32_t) * n_chunks,
                               cudaMemcpyHostToDevice, st));
     ENTE_CUDA(cudaMemsetAsync(w.ovf_n, 0, 2 * sizeof(int32_t), st));
+    if (w.rs_flag) ENTE_CUDA(cudaMemsetAsync(w.rs_flag, 0, sizeof(int32_t) * n_chunks, st));
     return ENTE_OK;
 }
 
@@ -1242,13 +1267,20 @@ static int search_impl(const double *pts64, int64_t total_rows, int dim, const e
                     resolve_kernel<<<nt, kWarpRefs, 0, st>>>(pts64, dim, w.info, w.tile0, n_chunks, k, p.lay,
                                                        w.perm, w.L, w.cnt3, w.ev, w.ev_n, ws_rows,
                                                        total_rows, out_eps, out_counts, w.ovf,
-                                                       w.ovf_n, w.rs, w.rs_n));
+                                                       w.ovf_n, w.rs, w.rs_n, w.rs_flag));
+        ENTE_CUDA(cudaGetLastError());
+        {
+            dim3 ggrid((unsigned)(p.max_npad / kTJ), (unsigned)std::min(n_chunks, 65535));
+            ENTE_LAUNCH("gather64", st,
+                        gather64_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.perm,
+                                                               w.rs_flag, w.pts64s));
+        }
         ENTE_CUDA(cudaGetLastError());
         {
             const unsigned rgrid = (unsigned)(num_sms() * 8);
             ENTE_LAUNCH("rescan", st,
                         rescan_table(p.dy, p.dx, k)<<<rgrid, kRescanWarps * 32, 0, st>>>(
-                            w.pts32, w.fbox, pts64, w.info, n_chunks, w.perm, w.t32, w.rs, w.rs_n,
+                            w.pts32, w.fbox, pts64, w.pts64s, w.info, n_chunks, w.perm, w.t32, w.rs, w.rs_n,
                             k, p.lay, total_rows, out_eps, out_counts));
         }
         ENTE_CUDA(cudaGetLastError());

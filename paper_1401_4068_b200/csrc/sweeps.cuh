@@ -870,10 +870,10 @@ constexpr int kRescanWarps = 4;
 template <int DY, int DX, int S>
 __global__ void __launch_bounds__(kRescanWarps * 32) rescan_kernel(
     const float *__restrict__ pts32, const float *__restrict__ fbox, const double *__restrict__ pts64,
-    const ChunkInfo *__restrict__ info, int n_chunks, const int32_t *__restrict__ perm,
-    const float *__restrict__ t32_in, const int64_t *__restrict__ list,
-    const int32_t *__restrict__ list_n, int k, TeLayout lay, int64_t total_rows,
-    double *__restrict__ out_eps, int32_t *__restrict__ out_counts) {
+    const double *__restrict__ pts64s, const ChunkInfo *__restrict__ info, int n_chunks,
+    const int32_t *__restrict__ perm, const float *__restrict__ t32_in,
+    const int64_t *__restrict__ list, const int32_t *__restrict__ list_n, int k, TeLayout lay,
+    int64_t total_rows, double *__restrict__ out_eps, int32_t *__restrict__ out_counts) {
     using L = Lay<DY, DX>;
     constexpr int D = L::D, DP = L::DP, NP = L::NP;
     constexpr int NG = DY < kGate ? DY : kGate;
@@ -894,7 +894,10 @@ __global__ void __launch_bounds__(kRescanWarps * 32) rescan_kernel(
         load_ref<D>(ref, cp + (int64_t)s * DP, true);
         double r64[D];
 #pragma unroll
-        for (int col = 0; col < D; ++col) r64[col] = pts64[row * D + col];
+        // fp64 rows in the count order (coalesced per sub-tile), written for
+        // every chunk with rescans by gather64_kernel
+        const double *s64 = pts64s + ci.prow0 * D;
+        for (int col = 0; col < D; ++col) r64[col] = s64[(int64_t)s * D + col];
         const double delta = ci.delta;
         const float hiA = __double2float_ru(__dadd_ru((double)t32_in[srow], 2.0 * delta));
         // ---- phase A: exact k-th joint distance
@@ -918,7 +921,7 @@ __global__ void __launch_bounds__(kRescanWarps * 32) rescan_kernel(
                     d = fmaxf(d, fabsf(q[col] + x));
                 }
                 if (lane < kSub && j < ci.n && j != s && d <= hiA) {
-                    const double *q64 = pts64 + (ci.row0 + perm[ci.row0 + j]) * D;
+                    const double *q64 = s64 + (int64_t)j * D;
                     double d64 = 0.0;
 #pragma unroll
                     for (int col = 0; col < D; ++col) d64 = fmax(d64, fabs(__dsub_rn(r64[col], q64[col])));
@@ -978,7 +981,7 @@ __global__ void __launch_bounds__(kRescanWarps * 32) rescan_kernel(
                 }
                 if (amb) {
                     double A, m2, m3, jd;
-                    te_dist64(r64, pts64 + (ci.row0 + perm[ci.row0 + j]) * D, D, DY, A, m2, m3, jd);
+                    te_dist64(r64, s64 + (int64_t)j * D, D, DY, A, m2, m3, jd);
                     const double v64[3] = {A, m2, m3};
 #pragma unroll
                     for (int o = 0; o < 3; ++o)
@@ -1005,9 +1008,9 @@ using CountFn = void (*)(const float *, const float *, const ChunkInfo *, const 
                          const float *, int64_t, int, int32_t *, uint32_t *, int32_t *, uint32_t,
                          unsigned long long *);
 
-using RescanFn = void (*)(const float *, const float *, const double *, const ChunkInfo *, int,
-                          const int32_t *, const float *, const int64_t *, const int32_t *, int,
-                          TeLayout, int64_t, double *, int32_t *);
+using RescanFn = void (*)(const float *, const float *, const double *, const double *,
+                          const ChunkInfo *, int, const int32_t *, const float *, const int64_t *,
+                          const int32_t *, int, TeLayout, int64_t, double *, int32_t *);
 
 
 // Every kernel of one compiled (d_y, d_x) TE layout.
