@@ -7,25 +7,28 @@
 // and fp64 certification of the few pairs the filter cannot decide:
 //
 //   prep      column mean / min / max, bound
-//             delta = 4 * 2^-24 * max|x - m| * (1 + 2^-20) >= |d32 - d64|
-//   sort      per-chunk Morton order over the filter columns (the y-past
-//             block: every contribution needs max|dy-past| inside the radius),
-//             CTA radix sort; fp32 copy x32 = fl32(x - m) in that order plus
-//             per-32 / per-128-row bounding boxes
-//   pruning   a warp (128 sorted references) skips a 32-candidate sub-tile
-//             when the fp32 box distance already exceeds its bound; boxes are
-//             exact lower bounds of every d32 in them, so skipping is exact
-//   pass 1    t32_i = k-th smallest fp32 distance (self excluded) via a
-//             (k+1)-slot sorted register list; L_i = #{d32 < lo_i}
-//   pass 2    per pair: the three TE marginal distances and the joint one;
-//             d32 < lo_i counts as certainly inside, values inside the band
-//             [lo_i, hi_i] = t32 -/+ 2 delta (directed rounding) are recorded
-//             as events (<= kCap per point)
+//             delta = 4 * 2^-24 * max|x - m| * (1 + 2^-20) >= |d32 - d64|,
+//             fp32 covariance -> principal axes (axes_kernel)
+//   orders    count order: Morton over the y-past gate columns; kNN order:
+//             Morton over the two principal axes when the chunk is
+//             essentially 2-D, else the count order (CTA radix sorts); fp32
+//             copies x32 = fl32(x - m) in both orders with per-32-row boxes
+//   pruning   a sweep warp (64 sorted references) skips a 32-candidate
+//             sub-tile when the fp32 box distance already exceeds its bound;
+//             boxes are exact lower bounds of every d32 in them
+//   pass 1    (sweeps.cuh) t32_i = k-th smallest fp32 distance (self
+//             excluded) via a (k+1)-slot sorted list; L_i = #{d32 < lo_i}
+//   pass 2    (sweeps.cuh) per pair: the three TE marginal distances and the
+//             joint one; d32 < lo_i counts as certainly inside, values in the
+//             band [lo_i, hi_i] = t32 -/+ 2 delta (directed rounding) are
+//             recorded as events (<= kCap per point)
 //   resolve   fp64 re-scoring of the events: eps_i = the (k - L_i)-th
 //             smallest joint d64 among band events; marginal events inside
 //             eps_i are added to the counts -> bit-identical to the reference
-//   exact     warp-per-point fp64 scan (overflowed points, chunks whose
-//             range defeats fp32, layouts without a compiled kernel)
+//   rescan    (sweeps.cuh) references whose events overflowed (ties): pruned
+//             warp walk with fp64 on every undecided candidate
+//   exact     warp-per-point fp64 scan (chunks whose range defeats fp32,
+//             layouts without a compiled sweep)
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
