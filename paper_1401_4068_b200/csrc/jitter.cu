@@ -136,10 +136,12 @@ __global__ void __launch_bounds__(kJitThreads) jitter_apply_kernel(double *__res
 
 // status: non-finite beats degenerate (np.ptp of a NaN column is NaN != 0);
 // one pass over the rows, per-thread column extrema (dim <= kMaxDim)
-__global__ void __launch_bounds__(256) check_kernel(const double *__restrict__ pts, int dim,
+template <int T>
+__global__ void __launch_bounds__(T) check_kernel(const double *__restrict__ pts, int dim,
                                                     const JitChunk *__restrict__ ch,
                                                     int32_t *__restrict__ status) {
-    __shared__ double wmin[8][kMaxDim], wmax[8][kMaxDim];
+    constexpr int NW = T / 32;
+    __shared__ double wmin[NW][kMaxDim], wmax[NW][kMaxDim];
     __shared__ int bad;
     const JitChunk c = ch[blockIdx.x];
     if (threadIdx.x == 0) bad = 0;
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(256) check_kernel(const double *__restrict__ p
             double ptp_max = 0.0;
             for (int q = 0; q < dim; ++q) {
                 double a = wmin[0][q], b = wmax[0][q];
-                for (int w = 1; w < 8; ++w) {
+                for (int w = 1; w < NW; ++w) {
                     a = fmin(a, wmin[w][q]);
                     b = fmax(b, wmax[w][q]);
                 }
@@ -270,7 +272,10 @@ extern "C" int ente_jitter(double *pts64, int dim, const ente_chunk *chunks, int
                                                                       n_chunks));
         ENTE_CUDA(cudaGetLastError());
     }
-    ENTE_LAUNCH("check", st, check_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.ch, status));
+    if (max_n <= 2048)  // small chunks: 64-thread CTAs, many per SM
+        ENTE_LAUNCH("check", st, check_kernel<64><<<n_chunks, 64, 0, st>>>(pts64, dim, w.ch, status));
+    else
+        ENTE_LAUNCH("check", st, check_kernel<256><<<n_chunks, 256, 0, st>>>(pts64, dim, w.ch, status));
     ENTE_CUDA(cudaGetLastError());
     return ENTE_OK;
 }

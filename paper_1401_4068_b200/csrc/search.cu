@@ -119,10 +119,12 @@ __device__ int principal_axes(double (&cov)[kPcaCols][kPcaCols], int P, float (&
 // (first group) the fp32 covariance about the chunk's first row for the
 // principal axes.  The mean only centres the fp32 copy and enters the error
 // bound through max|x - m|, so its summation order is free.
-constexpr int kPrepThreads = 256;
-constexpr int kPrepWarps = kPrepThreads / 32;
+constexpr int kPrepThreadsBig = 256;   // CTA size for chunks of > kPrepSmallN rows
+constexpr int kPrepThreadsSmall = 64;  // ... and for small chunks (C4: 500 rows)
+constexpr int kPrepSmallN = 2048;
 constexpr int kCovN = kPcaCols * (kPcaCols + 1) / 2;
 
+template <int kPrepThreads>
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double *__restrict__ pts64, int dim,
                                                             ChunkInfo *__restrict__ info,
                                                             ColStats *__restrict__ stats,
@@ -130,6 +132,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double *__rest
     const int c = blockIdx.x;
     const ChunkInfo ci = info[c];
     if (status[c] != ENTE_CHUNK_OK) return;
+    constexpr int kPrepWarps = kPrepThreads / 32;
     __shared__ double wred[3][kPrepWarps][8];
     __shared__ float wcov[kPrepWarps][kCovN];
     __shared__ ColStats local;
@@ -1091,7 +1094,9 @@ static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Pl
                          const SearchWs &w, int n_chunks, int32_t *status, int prune,
                          int allow_pca = 1) {
         ENTE_LAUNCH("prep", st,
-                    prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, w.stats, status, 1));
+                    (p.max_npad <= kPrepSmallN ? prep_kernel<kPrepThreadsSmall> : prep_kernel<kPrepThreadsBig>)
+                    <<<n_chunks, p.max_npad <= kPrepSmallN ? kPrepThreadsSmall : kPrepThreadsBig, 0, st>>>(
+                        pts64, dim, w.info, w.stats, status, 1));
         ENTE_CUDA(cudaGetLastError());
         ENTE_LAUNCH("axes", st,
                     axes_kernel<<<(n_chunks + 127) / 128, 128, 0, st>>>(w.info, n_chunks, dim, w.stats,
@@ -1292,7 +1297,7 @@ static int search_impl(const double *pts64, int64_t total_rows, int dim, const e
         ENTE_CUDA(cudaGetLastError());
     } else if (!p.fast && split_index == 0) {  // (a split search: part 0 does it all)
         ENTE_LAUNCH("prep", st,
-                    prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, nullptr, status, 0));
+                    prep_kernel<kPrepThreadsBig><<<n_chunks, kPrepThreadsBig, 0, st>>>(pts64, dim, w.info, nullptr, status, 0));
         ENTE_CUDA(cudaGetLastError());
         dispatch_exact(k, st, pts64, dim, w.info, n_chunks, status, nullptr, nullptr, total_rows,
                        masks, total_rows, out_eps, out_counts);
@@ -1369,7 +1374,7 @@ extern "C" int ente_knn_indices(const double *pts64, int64_t total_rows, int dim
         if (rc != ENTE_OK) return rc;
     } else {
         ENTE_LAUNCH("prep", st,
-                    prep_kernel<<<n_chunks, 256, 0, st>>>(pts64, dim, w.info, nullptr, status, 0));
+                    prep_kernel<kPrepThreadsBig><<<n_chunks, kPrepThreadsBig, 0, st>>>(pts64, dim, w.info, nullptr, status, 0));
         ENTE_CUDA(cudaGetLastError());
     }
     const float *p32 = p.fast ? w.pts32k : nullptr;
