@@ -93,9 +93,9 @@ __global__ void __launch_bounds__(32) jitter_std_kernel(const double *__restrict
 // Element e of a chunk (C order) takes the PCG64 output after step e + 1.
 // Threads own elements e0 + t + kJitThreads * i (coalesced); each advances
 // its state by kJitThreads steps with one precomputed affine LCG jump.
-constexpr int kJitThreads = 256;
 constexpr int kJitPerThread = 64;
 
+template <int kJitThreads>
 __global__ void __launch_bounds__(kJitThreads) jitter_apply_kernel(double *__restrict__ pts, int dim,
                                                                    const JitChunk *__restrict__ ch,
                                                                    const double *__restrict__ half_width,
@@ -264,12 +264,18 @@ extern "C" int ente_jitter(double *pts64, int dim, const ente_chunk *chunks, int
         ENTE_LAUNCH("jitter_std", st,
                     jitter_std_kernel<<<n_chunks, 32, 0, st>>>(pts64, dim, w.ch, amplitude, w.hw));
         ENTE_CUDA(cudaGetLastError());
-        const int64_t per_block = (int64_t)kJitThreads * kJitPerThread;
+        // small chunks: 64 threads, so the per-thread jump-ahead set-up is
+        // amortised over more elements
+        const int T = (int64_t)max_n * dim <= 64 * kJitPerThread ? 64 : 256;
+        const int64_t per_block = (int64_t)T * kJitPerThread;
         const int64_t gx = ((int64_t)max_n * dim + per_block - 1) / per_block;
         dim3 grid((unsigned)gx, (unsigned)(n_chunks < 65535 ? n_chunks : 65535));
-        ENTE_LAUNCH("jitter_apply", st,
-                    jitter_apply_kernel<<<grid, kJitThreads, 0, st>>>(pts64, dim, w.ch, w.hw,
-                                                                      n_chunks));
+        if (T == 64)
+            ENTE_LAUNCH("jitter_apply", st,
+                        jitter_apply_kernel<64><<<grid, 64, 0, st>>>(pts64, dim, w.ch, w.hw, n_chunks));
+        else
+            ENTE_LAUNCH("jitter_apply", st,
+                        jitter_apply_kernel<256><<<grid, 256, 0, st>>>(pts64, dim, w.ch, w.hw, n_chunks));
         ENTE_CUDA(cudaGetLastError());
     }
     if (max_n <= 2048)  // small chunks: 64-thread CTAs, many per SM
