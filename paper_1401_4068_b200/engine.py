@@ -28,6 +28,7 @@ from .exceptions import KTooLarge, ShapeMismatch
 MAX_DIM = 32   # column bitmasks are uint32 in the C ABI
 MAX_K = 64     # exact warp top-k merge keeps <= 64 slots per lane
 MAX_MARG = 8
+MAX_WAVE_ROWS = 1 << 27  # points per device wave of batch_search
 
 _workers = [os.cpu_count() or 1]
 
@@ -203,9 +204,19 @@ def batch_search(items: Sequence, k: int):
             continue
         groups.setdefault((dim, masks), []).append((slot, pts))
     for (dim, masks), members in groups.items():
-        outs = _run_group([p for _, p in members], dim, list(masks), k)
-        for (slot, _), res in zip(members, outs):
-            results[slot] = res
+        # device waves of at most MAX_WAVE_ROWS points (the search workspace is
+        # a few hundred bytes per point)
+        start = 0
+        while start < len(members):
+            stop, rows = start, 0
+            while stop < len(members) and (stop == start or rows + len(members[stop][1]) <= MAX_WAVE_ROWS):
+                rows += len(members[stop][1])
+                stop += 1
+            wave = members[start:stop]
+            outs = _run_group([p for _, p in wave], dim, list(masks), k)
+            for (slot, _), res in zip(wave, outs):
+                results[slot] = res
+            start = stop
     return results
 
 

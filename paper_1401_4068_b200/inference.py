@@ -28,8 +28,8 @@ from .embedding import EmbeddingSpec, PointSetBundle, check_assembly
 from .exceptions import EnteError, InvalidPermutation, KTooLarge, UnknownMethod
 from .ksg import _raise_status, te_chunks_device
 
-# rows per device wave (fp64 joint + fp32 copies + counts + events ~ 240 B/row)
-MAX_ROWS_PER_WAVE = 1 << 28
+# rows per device wave (fp64 joint + fp32 copies + counts + events + tie copy ~ 300 B/row: ~40 GB)
+MAX_ROWS_PER_WAVE = 1 << 27
 # a wave runs as up to SUB_BATCHES sub-batches on two streams (>= MIN_SUB_BATCH chunks each)
 SUB_BATCHES = int(os.environ.get("ENTE_SUB_BATCHES", "1"))
 MIN_SUB_BATCH = 64
