@@ -142,12 +142,14 @@ __device__ __forceinline__ Band make_band(float t32, double delta) {
     const double two = 2.0 * delta;
     const float lo = __double2float_rd(__dsub_rd((double)t32, two));
     const float hi = __double2float_ru(__dadd_ru((double)t32, two));
-    const double w = fmax(__dsub_ru((double)t32, (double)lo), __dsub_ru((double)hi, (double)t32));
     b.lo = lo;
     b.hi = hi;
     b.nlo = -lo;
     b.nt = -t32;
-    b.w = __double2float_ru(w);
+    // band width, rounded up: v in [lo, hi] => 0 <= fl(v - lo) <= w, so the
+    // sweeps test |fl(v - lo)| <= w on the values they already subtract for
+    // the counts (a superset: the exact flags are recomputed on a hit)
+    b.w = __fsub_ru(hi, lo);
     return b;
 }
 
@@ -572,14 +574,12 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
                 const float jd = fmaxf(m2, m3);
                 // certain-inside counts: sign bit of (v - lo)
                 const float2 e = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nlo, band[r].nlo));
-                const float e3 = m3 + band[r].nlo;
+                const float2 e34 = __fadd2_rn(make_float2(m3, jd), make_float2(band[r].nlo, band[r].nlo));
                 cA[r] += __float_as_uint(e.x) >> 31;
                 c2[r] += __float_as_uint(e.y) >> 31;
-                c3[r] += __float_as_uint(e3) >> 31;
-                // conservative band test: min |v - t| <= w
-                const float2 b1 = __fadd2_rn(make_float2(A, m2), make_float2(band[r].nt, band[r].nt));
-                const float2 b2 = __fadd2_rn(make_float2(m3, jd), make_float2(band[r].nt, band[r].nt));
-                const float bm = fminf(fminf(fabsf(b1.x), fabsf(b1.y)), fminf(fabsf(b2.x), fabsf(b2.y)));
+                c3[r] += __float_as_uint(e34.x) >> 31;
+                // conservative band test on the same differences: min |v - lo| <= w
+                const float bm = fminf(fminf(fabsf(e.x), fabsf(e.y)), fminf(fabsf(e34.x), fabsf(e34.y)));
                 if (bm <= band[r].w) {
                     const float lo = band[r].lo, hi = band[r].hi;
                     uint32_t f = ((A >= lo && A <= hi) ? 1u : 0u) | ((m2 >= lo && m2 <= hi) ? 2u : 0u) |
@@ -746,7 +746,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
             }
             const float lo = active ? rs.lo[ri] : -INFINITY;
             const float hi = active ? rs.hi[ri] : -INFINITY;
-            const float nlo = -lo, nt = rs.t[ri], wb = active ? rs.w[ri] : -1.0f;
+            const float nlo = -lo, wb = active ? rs.w[ri] : -1.0f;
             uint32_t cA = 0u, c2 = 0u, c3 = 0u;
             int nev = active ? rs.nev[ri] : 0;
             const int64_t evrow = (ci.row0 + wrow + ri) * kCap;
@@ -762,13 +762,12 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
                 const float m3 = maxabs<1 + DY, D, 2 * NP>(a, A);
                 const float jd = fmaxf(m2, m3);
                 const float2 e = __fadd2_rn(make_float2(A, m2), make_float2(nlo, nlo));
-                const float e3 = m3 + nlo;
+                const float2 e34 = __fadd2_rn(make_float2(m3, jd), make_float2(nlo, nlo));
                 cA += __float_as_uint(e.x) >> 31;
                 c2 += __float_as_uint(e.y) >> 31;
-                c3 += __float_as_uint(e3) >> 31;
-                const float2 b1 = __fadd2_rn(make_float2(A, m2), make_float2(nt, nt));
-                const float2 b2 = __fadd2_rn(make_float2(m3, jd), make_float2(nt, nt));
-                const float bm = fminf(fminf(fabsf(b1.x), fabsf(b1.y)), fminf(fabsf(b2.x), fabsf(b2.y)));
+                c3 += __float_as_uint(e34.x) >> 31;
+                // conservative band test on the same differences: min |v - lo| <= w
+                const float bm = fminf(fminf(fabsf(e.x), fabsf(e.y)), fminf(fabsf(e34.x), fabsf(e34.y)));
                 if (bm <= wb) {
                     uint32_t f = ((A >= lo && A <= hi) ? 1u : 0u) | ((m2 >= lo && m2 <= hi) ? 2u : 0u) |
                                  ((m3 >= lo && m3 <= hi) ? 4u : 0u) | ((jd >= lo && jd <= hi) ? 8u : 0u);
