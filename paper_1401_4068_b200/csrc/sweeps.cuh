@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace ente {
@@ -27,6 +29,9 @@ constexpr int kGate = 4;                    // gate columns in the Morton key an
 #endif
 #ifndef ENTE_CNT_NSLOT
 #define ENTE_CNT_NSLOT 2
+#endif
+#ifndef ENTE_CNT_GROUPS
+#define ENTE_CNT_GROUPS 1  // grouped count rounds (several lanes per reference for small rounds)
 #endif
 #ifndef ENTE_CNT_MINB
 #define ENTE_CNT_MINB 32
@@ -300,6 +305,7 @@ __device__ __forceinline__ float point_box(const float2 (&nr)[NP], const Box<Q> 
 template <int DP, int NSLOT>
 struct Ring {
     float buf[NSLOT][kSub * DP];
+    float spill[4 * DP];  // read (never used) by the count pass's last row prefetch
     uint64_t full[NSLOT];
 };
 
@@ -661,7 +667,6 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
     const float *cp = pts32 + ci.prow0 * DP;
     const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2;
     const int wrow = tr.r0;
-    float2 myref[kRT][NP];  // this lane's own references (walker tests)
     float myhi[kRT];
     float hmax = 0.0f;
 #pragma unroll
@@ -669,7 +674,6 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
         const int ri = r * 32 + lane;
         const int idx = wrow + ri;
         const bool valid = idx < ci.n;
-        load_ref<D>(myref[r], cp + (int64_t)idx * DP, valid);
 #pragma unroll
         for (int c = 0; c < DP; ++c) rs.ref[ri][c] = (valid && c < D) ? cp[(int64_t)idx * DP + c] : 0.0f;
         Band b = make_band(valid ? t32_in[ci.row0 + idx] : 0.0f, ci.delta);
@@ -691,11 +695,26 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
     }
     const float bound = warp_max_nonneg(hmax);
     constexpr int NG = DY < kGate ? DY : kGate;
+    // this lane's own references' gate columns (negated, packed), read back
+    // from shared memory so they hold no registers through the rounds
+    struct NegRef {
+        float2 v[NP];
+    };
+    auto gate_ref = [&](int r) {
+        NegRef nr;
+        const float2 *rr = reinterpret_cast<const float2 *>(rs.ref[r * 32 + lane]);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const float2 v = p <= NG / 2 ? rr[p] : make_float2(0.0f, 0.0f);
+            nr.v[p] = make_float2(-v.x, -v.y);
+        }
+        return nr;
+    };
     auto refs_need = [&](const Box<1> &b) {
         uint32_t need = 0u;
 #pragma unroll
         for (int r = 0; r < kRT; ++r)
-            need |= ((!prune && myhi[r] > -INFINITY) || point_box<1, NG, NP, 1>(myref[r], b) <= myhi[r])
+            need |= ((!prune && myhi[r] > -INFINITY) || point_box<1, NG, NP, 1>(gate_ref(r).v, b) <= myhi[r])
                         ? (1u << r) : 0u;
         return need;
     };
@@ -732,9 +751,18 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
         mbar_wait(&ring.full[slot], (uint32_t)(used / NSLOT) & 1u);
         const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[slot]);
         constexpr int NQ = DP / 4;
-        for (int round = 0; round < nneed; round += 32) {
-            const bool active = round + lane < nneed;
-            const int ri = active ? rs.slot[round + lane] : 0;
+        // Grouped rounds: with at most 8 (16) references left, the warp splits
+        // into 4 (2) groups of lanes that share the round's references and
+        // take every 4th (2nd) candidate row, so the round walks 8 (16) rows
+        // instead of 32 (half the rounds hold <= 8 references).  LG = log2 of
+        // the group count is a compile-time constant of each specialisation.
+        auto run_round = [&](auto lgc, int round) {
+            constexpr int LG = decltype(lgc)::value;
+            constexpr int G = 1 << LG, PER = 32 >> LG, STRIDE = G * NQ;
+            const int g = lane >> (5 - LG);  // group: candidate rows g, g + G, g + 2G, ...
+            const int it = lane & (PER - 1);
+            const bool active = round + it < nneed;
+            const int ri = active ? rs.slot[round + it] : 0;
             float2 ref[NP];
             {
                 const float2 *rr = reinterpret_cast<const float2 *>(rs.ref[ri]);
@@ -748,9 +776,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
             const float hi = active ? rs.hi[ri] : -INFINITY;
             const float nlo = -lo, wb = active ? rs.w[ri] : -1.0f;
             uint32_t cA = 0u, c2 = 0u, c3 = 0u;
-            int nev = active ? rs.nev[ri] : 0;
-            const int64_t evrow = (ci.row0 + wrow + ri) * kCap;
-            // one candidate row against this lane's reference
+            // one candidate row (sub-tile row j) against this lane's reference
             auto visit = [&](const float4 (&cur)[NQ], int j) {
                 const float2 *c = reinterpret_cast<const float2 *>(cur);
                 float a[2 * NP];
@@ -772,33 +798,49 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
                     uint32_t f = ((A >= lo && A <= hi) ? 1u : 0u) | ((m2 >= lo && m2 <= hi) ? 2u : 0u) |
                                  ((m3 >= lo && m3 <= hi) ? 4u : 0u) | ((jd >= lo && jd <= hi) ? 8u : 0u);
                     f &= fmask;
-                    if (f) {
-                        if (nev < kCap) ev[evrow + nev] = (uint32_t)(cur_st * kSub + j) | (f << 28);
-                        ++nev;
+                    if (f) {  // rare; the groups of one round share references
+                        const int pos = atomicAdd(&rs.nev[ri], 1);
+                        if (pos < kCap)
+                            ev[(ci.row0 + wrow + ri) * kCap + pos] = (uint32_t)(cur_st * kSub + j) | (f << 28);
                     }
                 }
             };
             // ping-pong row registers: the next row's LDS overlaps this row's math
+            const float4 *pr = tile + g * NQ;  // this lane's row s (loop-carried)
             float4 ra[NQ], rb[NQ];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) ra[q] = tile[q];
-            for (int j = 0; j < kSub; j += 2) {
+            for (int q = 0; q < NQ; ++q) ra[q] = pr[q];
+            for (int s = 0; s < PER; s += 2, pr += 2 * STRIDE) {
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) rb[q] = tile[(j + 1) * NQ + q];
-                visit(ra, j);
-                if (j + 2 < kSub) {
+                for (int q = 0; q < NQ; ++q) rb[q] = pr[STRIDE + q];
+                visit(ra, s * G + g);
+                // the last iteration reads G rows past the slot (Ring::spill)
 #pragma unroll
-                    for (int q = 0; q < NQ; ++q) ra[q] = tile[(j + 2) * NQ + q];
-                }
-                visit(rb, j + 1);
+                for (int q = 0; q < NQ; ++q) ra[q] = pr[2 * STRIDE + q];
+                visit(rb, (s + 1) * G + g);
             }
-            if (active) {
+            // fold the groups' counts onto group 0
+#pragma unroll
+            for (int o = PER; o < 32; o <<= 1) {
+                cA += __shfl_xor_sync(0xffffffffu, cA, o);
+                c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+                c3 += __shfl_xor_sync(0xffffffffu, c3, o);
+            }
+            if (active && g == 0) {
                 rs.cnt[0][ri] += cA;
                 rs.cnt[1][ri] += c2;
                 rs.cnt[2][ri] += c3;
-                rs.nev[ri] = nev;
             }
             __syncwarp();
+        };
+        for (int round = 0; round < nneed; round += 32) {
+            const int m = nneed - round;
+            if (ENTE_CNT_GROUPS && m <= 8)
+                run_round(std::integral_constant<int, 2>{}, round);
+            else if (ENTE_CNT_GROUPS && m <= 16)
+                run_round(std::integral_constant<int, 1>{}, round);
+            else
+                run_round(std::integral_constant<int, 0>{}, round);
         }
         ++nsub;
         __syncwarp();
