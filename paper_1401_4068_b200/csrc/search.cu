@@ -838,9 +838,19 @@ __global__ void __launch_bounds__(kIdxWarps * 32) knn_index_kernel(
 // ---------------------------------------------------------------------------
 // Layout tables: the sweeps of every compiled (d_y, d_x) live in the
 // sweeps_*.cu translation units (sweeps.cuh).
-static KnnFn knn_table(int dy, int dx, int slots) {
+// Chunks of a few sub-tiles: nearly every reference needs every sub-tile,
+// so compaction only adds its overhead; the direct two-per-lane sweeps win.
+constexpr int kCompactMinRows = 4096;
+
+#ifndef ENTE_KNN_COMPACT
+#define ENTE_KNN_COMPACT 1
+#endif
+
+static KnnFn knn_table(int dy, int dx, int slots, int max_npad = 0) {
     SweepSet ss;
     if (!find_sweep_set(dy, dx, ss)) return nullptr;
+    if (ENTE_KNN_COMPACT && max_npad >= kCompactMinRows && slots <= 16)
+        return slots <= 5 ? ss.knn_compact[0] : slots <= 8 ? ss.knn_compact[1] : ss.knn_compact[2];
     return slots <= 5 ? ss.knn[0] : slots <= 8 ? ss.knn[1] : slots <= 16 ? ss.knn[2]
          : slots <= 32 ? ss.knn[3] : slots <= 64 ? ss.knn[4] : nullptr;
 }
@@ -851,10 +861,6 @@ static RescanFn rescan_table(int dy, int dx, int k) {
     return k <= 4 ? ss.rescan[0] : k <= 8 ? ss.rescan[1] : k <= 16 ? ss.rescan[2]
          : k <= 32 ? ss.rescan[3] : ss.rescan[4];
 }
-
-// Chunks of a few sub-tiles: nearly every reference needs every sub-tile,
-// so compaction only adds its overhead; the direct two-per-lane sweep wins.
-constexpr int kCompactMinRows = 4096;
 
 static CountFn count_table(int dy, int dx, int max_npad) {
     SweepSet ss;
@@ -1260,7 +1266,7 @@ static int search_impl(const double *pts64, int64_t total_rows, int dim, const e
                                   cudaMemcpyHostToDevice, st));
         const unsigned nt = (unsigned)ntiles;
         ENTE_LAUNCH("knn_pass", st,
-                    knn_table(p.dy, p.dx, p.slots)<<<nt, 32, 0, st>>>(w.pts32k, w.fboxk, w.info,
+                    knn_table(p.dy, p.dx, p.slots, p.max_npad)<<<nt, 32, 0, st>>>(w.pts32k, w.fboxk, w.info,
                                                                      w.tile0, n_chunks, k, prune, w.kmap, w.t32,
                                                                      w.L, work));
         ENTE_CUDA(cudaGetLastError());

@@ -31,7 +31,13 @@ constexpr int kGate = 4;                    // gate columns in the Morton key an
 #define ENTE_CNT_NSLOT 2
 #endif
 #ifndef ENTE_CNT_GROUPS
-#define ENTE_CNT_GROUPS 1  // grouped count rounds (several lanes per reference for small rounds)
+#define ENTE_CNT_GROUPS 2  // grouped count rounds: 0 off, 1 up to 4 groups, 2 up to 8 groups
+#endif
+#ifndef ENTE_KNNC_NSLOT
+#define ENTE_KNNC_NSLOT 2  // ring slots of the compacted kNN pass
+#endif
+#ifndef ENTE_KNNC_REGREF
+#define ENTE_KNNC_REGREF 1  // compacted kNN: walker tests from register copies of the lane's refs
 #endif
 #ifndef ENTE_CNT_MINB
 #define ENTE_CNT_MINB 32
@@ -305,7 +311,7 @@ __device__ __forceinline__ float point_box(const float2 (&nr)[NP], const Box<Q> 
 template <int DP, int NSLOT>
 struct Ring {
     float buf[NSLOT][kSub * DP];
-    float spill[4 * DP];  // read (never used) by the count pass's last row prefetch
+    float spill[8 * DP];  // read (never used) by the count pass's last row prefetch
     uint64_t full[NSLOT];
 };
 
@@ -465,6 +471,237 @@ __global__ void __launch_bounds__(32, S > 16 ? 24 : (S > 8 ? 16 : sweep_minb(1 +
 #pragma unroll
             for (int s = 0; s < S; ++s) Lc += (kd[r][s] > -INFINITY) && (kd[r][s] < lo);
         }
+        if (lo > 0.0f) Lc -= 1;  // the self pair (distance 0) was counted
+        const int64_t orow = ci.row0 + (kmap ? kmap[ci.row0 + idx] : idx);  // count-order row
+        t32_out[orow] = t32;
+        L_out[orow] = Lc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// pass 1, compacted references (chunks >= kCompactMinRows, k + 1 <= 16).
+//
+// Same walk, boxes and result as knn_pass_kernel, organised like the count
+// pass: the warp's 64 references and their sorted lists live in shared
+// memory; for every streamed sub-tile only the references whose point-to-box
+// distance is below their current k-th distance (about a quarter of them on
+// embedded dynamics) ride the lanes, in grouped rounds (<= 8 / <= 16
+// references: 4 / 2 lane groups over interleaved candidate rows).  A lane of
+// group g > 0 starts from an empty list bounded by the reference's current
+// k-th distance; at the end of the round the groups' lists are merged into
+// group 0 by a shuffle tree (only when some lane found a closer row).
+// ---------------------------------------------------------------------------
+template <int DP, int S>
+struct KnnRefs {
+    float ref[32 * kRT][DP];  // fp32 centred coordinates
+    float kd[S][32 * kRT];    // ascending lists ([slot][reference]: conflict-free)
+    int slot[32 * kRT];       // compacted reference list of the current sub-tile
+};
+
+template <int DY, int DX, int S>
+__global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) knn_compact_kernel(
+    const float *__restrict__ pts32, const float *__restrict__ fbox,
+    const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks, int k, int prune,
+    const int32_t *__restrict__ kmap, float *__restrict__ t32_out, int32_t *__restrict__ L_out,
+    unsigned long long *__restrict__ work) {
+    static_assert(S <= 16, "register lists only");
+    using L = Lay<DY, DX>;
+    constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG;
+    constexpr int NSLOT = ENTE_KNNC_NSLOT;
+    constexpr int NBC = D < 4 * kKnnQ ? D : 4 * kKnnQ;  // box columns 0 .. NBC-1
+    constexpr int GC = 2 * PG < D ? 2 * PG : D;          // gate columns 0 .. GC-1
+    constexpr int NQ = DP / 4;
+    __shared__ __align__(128) Ring<DP, NSLOT> ring;
+    __shared__ __align__(16) KnnRefs<DP, S> rs;
+    const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
+    const ChunkInfo ci = info[tr.chunk];
+    if (!ci.ok32) return;
+    const int lane = threadIdx.x;
+    const unsigned lt = (1u << lane) - 1u;
+    const float *cp = pts32 + ci.prow0 * DP;
+    const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2 * kKnnQ;
+    const int wrow = tr.r0;
+#pragma unroll
+    for (int r = 0; r < kRT; ++r) {
+        const int ri = r * 32 + lane;
+        const int idx = wrow + ri;
+        const bool valid = idx < ci.n;
+#pragma unroll
+        for (int c = 0; c < DP; ++c) rs.ref[ri][c] = (valid && c < D) ? cp[(int64_t)idx * DP + c] : 0.0f;
+#pragma unroll
+        for (int s = 0; s < S; ++s) rs.kd[s][ri] = (!valid || s < S - (k + 1)) ? -INFINITY : INFINITY;
+    }
+#if ENTE_KNNC_REGREF
+    // this lane's own references and current k-th distances in registers
+    // (walker tests); the k-th values are refreshed after every sub-tile
+    float2 myref[kRT][NP];
+    float mythr[kRT];
+#pragma unroll
+    for (int r = 0; r < kRT; ++r) {
+        const int idx = wrow + r * 32 + lane;
+        load_ref<D>(myref[r], cp + (int64_t)idx * DP, idx < ci.n);
+        mythr[r] = idx < ci.n ? INFINITY : -INFINITY;
+    }
+#endif
+    // this lane's references: point-to-box tests against their current k-th
+    auto refs_need = [&](const Box<kKnnQ> &b) {
+        uint32_t need = 0u;
+#pragma unroll
+        for (int r = 0; r < kRT; ++r) {
+#if ENTE_KNNC_REGREF
+            const float thr = mythr[r];
+            const float2 (&nr)[NP] = myref[r];
+#else
+            const int ri = r * 32 + lane;
+            const float thr = rs.kd[S - 1][ri];
+            float2 nr[NP];
+            const float2 *rr = reinterpret_cast<const float2 *>(rs.ref[ri]);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) nr[p] = make_float2(-rr[p].x, -rr[p].y);
+#endif
+            need |= (thr > -INFINITY && (!prune || point_box<0, NBC, NP, kKnnQ>(nr, b) < thr)) ? (1u << r) : 0u;
+        }
+        return need;
+    };
+    auto warp_bound = [&]() {
+        float wb = 0.0f;
+#pragma unroll
+        for (int r = 0; r < kRT; ++r) {
+            const float t = rs.kd[S - 1][r * 32 + lane];
+#if ENTE_KNNC_REGREF
+            mythr[r] = t;
+#endif
+            wb = fmaxf(wb, t);
+        }
+        return warp_max_nonneg(wb);
+    };
+    if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
+    fence_barrier_init();
+    __syncwarp();
+    Walker<kKnnQ> wk;
+    wk.init(fb, wrow, ci.n, ci.npad);
+    float bound = INFINITY;  // warp max of the current k-th distances
+    int slot_st = -1;
+    uint32_t slot_need = 0u;
+    int issued = 0;
+    uint32_t nsub = 0;
+    for (; issued < NSLOT; ++issued) {
+        const int st = wk.next(fb, prune ? bound : INFINITY, true, refs_need);
+        if (st < 0) break;
+        if (lane == issued) slot_st = st;
+        slot_need |= wk.need << (kRT * issued);
+        if (lane == 0) ring_issue(ring, issued, cp + (int64_t)st * kSub * DP);
+    }
+    for (int used = 0; used < issued; ++used) {
+        const int slot = used % NSLOT;
+        const uint32_t nb = (slot_need >> (kRT * slot)) & ((1u << kRT) - 1u);
+        int base = 0;
+#pragma unroll
+        for (int r = 0; r < kRT; ++r) {
+            const uint32_t m = __ballot_sync(0xffffffffu, (nb >> r) & 1u);
+            if ((nb >> r) & 1u) rs.slot[base + __popc(m & lt)] = r * 32 + lane;
+            base += __popc(m);
+        }
+        const int nneed = base;
+        __syncwarp();
+        mbar_wait(&ring.full[slot], (uint32_t)(used / NSLOT) & 1u);
+        const float4 *tile = reinterpret_cast<const float4 *>(ring.buf[slot]);
+        auto run_round = [&](auto lgc, int round) {
+            constexpr int LG = decltype(lgc)::value;
+            constexpr int G = 1 << LG, PER = 32 >> LG, STRIDE = G * NQ;
+            const int g = lane >> (5 - LG);
+            const int it = lane & (PER - 1);
+            const bool active = round + it < nneed;
+            const int ri = active ? rs.slot[round + it] : 0;
+            float2 ref[NP];
+            {
+                const float2 *rr = reinterpret_cast<const float2 *>(rs.ref[ri]);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) ref[p] = make_float2(-rr[p].x, -rr[p].y);
+            }
+            float kd[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) kd[s] = !active ? -INFINITY : (g == 0 ? rs.kd[s][ri] : INFINITY);
+            float thr = active ? rs.kd[S - 1][ri] : -INFINITY;  // rows at or beyond it cannot enter
+            auto visit = [&](const float4 (&cur)[NQ]) {
+                const float2 *c = reinterpret_cast<const float2 *>(cur);
+                float a[2 * NP];
+                diff_pairs<D, 0, PG>(ref, c, a);
+                float dj = maxabs0<0, GC, 2 * NP>(a);
+                if (!__any_sync(0xffffffffu, dj < thr)) return;
+                diff_pairs<D, PG, NP>(ref, c, a);
+                dj = maxabs<GC, D, 2 * NP>(a, dj);
+                if (dj < thr) {
+                    insert_sorted<S>(kd, dj);
+                    thr = fminf(thr, kd[S - 1]);
+                }
+            };
+            const float4 *pr = tile + g * NQ;
+            float4 ra[NQ], rb[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) ra[q] = pr[q];
+            for (int s = 0; s < PER; s += 2, pr += 2 * STRIDE) {
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) rb[q] = pr[STRIDE + q];
+                visit(ra);
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) ra[q] = pr[2 * STRIDE + q];  // may read Ring::spill
+                visit(rb);
+            }
+            // merge the groups' lists into group 0 (tree; lists are ascending)
+#pragma unroll
+            for (int o = 16; o >= PER; o >>= 1) {
+                const float p0 = __shfl_xor_sync(0xffffffffu, kd[0], o);
+                const bool recv = (lane & o) == 0;
+                if (__any_sync(0xffffffffu, recv && p0 < kd[S - 1])) {
+                    float pv[S];
+#pragma unroll
+                    for (int s = 0; s < S; ++s) pv[s] = __shfl_xor_sync(0xffffffffu, kd[s], o);
+                    if (recv) {
+#pragma unroll
+                        for (int s = 0; s < S; ++s) insert_sorted<S>(kd, pv[s]);
+                    }
+                }
+            }
+            if (active && g == 0) {
+#pragma unroll
+                for (int s = 0; s < S; ++s) rs.kd[s][ri] = kd[s];
+            }
+            __syncwarp();
+        };
+        for (int round = 0; round < nneed; round += 32) {
+            const int m = nneed - round;
+            if (m <= 8)
+                run_round(std::integral_constant<int, 2>{}, round);
+            else if (m <= 16)
+                run_round(std::integral_constant<int, 1>{}, round);
+            else
+                run_round(std::integral_constant<int, 0>{}, round);
+        }
+        ++nsub;
+        bound = warp_bound();
+        const int st = wk.next(fb, prune ? bound : INFINITY, true, refs_need);
+        if (st >= 0) {
+            const int ns = issued % NSLOT;
+            if (lane == ns) slot_st = st;
+            slot_need = (slot_need & ~(((1u << kRT) - 1u) << (kRT * ns))) | (wk.need << (kRT * ns));
+            if (lane == 0) ring_issue(ring, ns, cp + (int64_t)st * kSub * DP);
+            ++issued;
+        }
+    }
+    (void)slot_st;
+    if (lane == 0) atomicAdd(work, (unsigned long long)nsub);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < kRT; ++r) {
+        const int ri = r * 32 + lane;
+        const int idx = wrow + ri;
+        if (idx >= ci.n) continue;
+        const float t32 = rs.kd[S - 1][ri];
+        const float lo = __double2float_rd(__dsub_rd((double)t32, 2.0 * ci.delta));
+        int Lc = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) Lc += (rs.kd[s][ri] > -INFINITY) && (rs.kd[s][ri] < lo);
         if (lo > 0.0f) Lc -= 1;  // the self pair (distance 0) was counted
         const int64_t orow = ci.row0 + (kmap ? kmap[ci.row0 + idx] : idx);  // count-order row
         t32_out[orow] = t32;
@@ -835,7 +1072,9 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
         };
         for (int round = 0; round < nneed; round += 32) {
             const int m = nneed - round;
-            if (ENTE_CNT_GROUPS && m <= 8)
+            if (ENTE_CNT_GROUPS > 1 && m <= 4)
+                run_round(std::integral_constant<int, 3>{}, round);
+            else if (ENTE_CNT_GROUPS && m <= 8)
                 run_round(std::integral_constant<int, 2>{}, round);
             else if (ENTE_CNT_GROUPS && m <= 16)
                 run_round(std::integral_constant<int, 1>{}, round);
@@ -1057,6 +1296,7 @@ using RescanFn = void (*)(const float *, const float *, const double *, const do
 // Every kernel of one compiled (d_y, d_x) TE layout.
 struct SweepSet {
     KnnFn knn[5];      // k + 1 <= 5, 8, 16 register slots; 32, 64 shared-memory slots
+    KnnFn knn_compact[3];  // k + 1 <= 5, 8, 16, compacted references (chunks >= 4096 rows)
     CountFn compact;   // count pass, compacted references (chunks >= 4096 rows)
     CountFn direct;    // count pass, two references per lane (small chunks)
     RescanFn rescan[5];  // k <= 4, 8, 16, 32, 64
@@ -1070,6 +1310,9 @@ SweepSet make_sweep_set() {
     s.knn[2] = knn_pass_kernel<DY, DX, 16>;
     s.knn[3] = knn_pass_kernel<DY, DX, 32>;
     s.knn[4] = knn_pass_kernel<DY, DX, 64>;
+    s.knn_compact[0] = knn_compact_kernel<DY, DX, 5>;
+    s.knn_compact[1] = knn_compact_kernel<DY, DX, 8>;
+    s.knn_compact[2] = knn_compact_kernel<DY, DX, 16>;
     s.compact = count_pass_kernel<DY, DX>;
     s.direct = count_pass_direct_kernel<DY, DX>;
     s.rescan[0] = rescan_kernel<DY, DX, 4>;

@@ -70,3 +70,35 @@ def test_mixed_batch_one_call(seed):
         eps, cnt = oracle.search(p, margs, 4)
         assert np.array_equal(r.kth_distance, eps)
         assert all(np.array_equal(a, b) for a, b in zip(r.radius_counts, cnt))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_compacted_sweeps_bit_exact(seed):
+    """Batches whose largest chunk has >= 4096 rows take the compacted kNN and
+    count sweeps (grouped rounds); random k over all three register-list
+    widths (k + 1 <= 5, 8, 16), ties, smooth embedded data and clusters."""
+    rng = np.random.default_rng(500 + seed)
+    dim = int(rng.choice([3, 5, 7, 9]))
+    dy = int(rng.integers(1, dim - 1))
+    margs = [list(range(1, 1 + dy)), list(range(0, 1 + dy)), list(range(1, dim))]
+    k = int(rng.choice([1, 4, 6, 11, 15]))
+    chunks = []
+    for kind in range(4):
+        n = int(rng.integers(4096, 9000)) if kind == 0 else int(rng.integers(300, 7000))
+        if kind == 1:
+            p = np.round(rng.standard_normal((n, dim)), 1)
+        elif kind == 2:
+            s = np.cumsum(rng.standard_normal(n + dim))
+            p = np.stack([s[i:i + n] for i in range(dim)], axis=1)
+        elif kind == 3:
+            c = rng.standard_normal((8, dim)) * 5.0
+            p = c[rng.integers(0, 8, n)] + 0.05 * rng.standard_normal((n, dim))
+        else:
+            p = rng.standard_normal((n, dim))
+        chunks.append(p)
+    res = batch_search([(Chunk(p), margs) for p in chunks], k)
+    for p, r in zip(chunks, res):
+        assert not isinstance(r, Exception), r
+        eps, cnt = oracle.search(p, margs, k)
+        assert np.array_equal(r.kth_distance, eps), (p.shape, k)
+        assert all(np.array_equal(a, b) for a, b in zip(r.radius_counts, cnt)), (p.shape, k)
