@@ -12,7 +12,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${tag}_launches.csv python bench.py --config $cfg --steps 1 --warmup 3 --no-e2e --no-cpu \
     > gpurun_out/${tag}_launches.log 2>&1
 echo "launches rc=$?"
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:'knn_pass|count_pass' -c 2 \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:'knn_pass|knn_compact|count_pass' -c 2 \
     -o gpurun_out/${tag}_prof -f python bench.py --config $cfg --steps 1 --warmup 1 --no-e2e --no-cpu \
     > gpurun_out/${tag}_ncu.log 2>&1
 echo "ncu rc=$?"; tail -3 gpurun_out/${tag}_ncu.log

@@ -17,7 +17,10 @@ if "--traffic" in sys.argv:  # {kernel: dram read+write bytes per launch} for be
     res = {}
     for r in rows[2:]:
         d = dict(zip(hdr, r))
-        name = d["Kernel Name"].split("<")[0].replace("void ", "").split("(")[0].strip()
+        name = d["Kernel Name"].split("<")[0].replace("void ", "").split("(")[0].strip().split("::")[-1]
+        # launch labels of bench.py's kernel profile (the compacted kNN sweep is "knn_pass")
+        name = {"knn_pass_kernel": "knn_pass", "knn_compact_kernel": "knn_pass",
+                "count_pass_kernel": "count_pass", "count_pass_direct_kernel": "count_pass"}.get(name, name)
         tot = 0.0
         for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             tot += float(d[k].replace(",", "")) * scale.get(units[hdr.index(k)], 1)
