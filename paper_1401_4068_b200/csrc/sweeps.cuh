@@ -39,6 +39,17 @@ constexpr int kGate = 4;                    // gate columns in the Morton key an
 #ifndef ENTE_KNNC_REGREF
 #define ENTE_KNNC_REGREF 1  // compacted kNN: walker tests from register copies of the lane's refs
 #endif
+#define ENTE_PRAGMA(x) _Pragma(#x)
+#define ENTE_UNROLL(n) ENTE_PRAGMA(unroll n)
+#ifndef ENTE_CNT_BANDVOTE
+#define ENTE_CNT_BANDVOTE 0  // count pass: band test as a warp vote
+#endif
+#ifndef ENTE_CNT_UNROLL
+#define ENTE_CNT_UNROLL 2    // count pass: row-pair iterations unrolled per loop trip
+#endif
+#ifndef ENTE_KNNC_UNROLL
+#define ENTE_KNNC_UNROLL 1   // compacted kNN pass: row-pair iterations per loop trip
+#endif
 #ifndef ENTE_CNT_MINB
 #define ENTE_CNT_MINB 32
 #endif
@@ -640,6 +651,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) kn
             float4 ra[NQ], rb[NQ];
 #pragma unroll
             for (int q = 0; q < NQ; ++q) ra[q] = pr[q];
+ENTE_UNROLL(ENTE_KNNC_UNROLL)
             for (int s = 0; s < PER; s += 2, pr += 2 * STRIDE) {
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) rb[q] = pr[STRIDE + q];
@@ -1031,7 +1043,11 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
                 c3 += __float_as_uint(e34.x) >> 31;
                 // conservative band test on the same differences: min |v - lo| <= w
                 const float bm = fminf(fminf(fabsf(e.x), fabsf(e.y)), fminf(fabsf(e34.x), fabsf(e34.y)));
+#if ENTE_CNT_BANDVOTE
+                if (__any_sync(0xffffffffu, bm <= wb)) {  // warp-uniform: no reconvergence stack
+#else
                 if (bm <= wb) {
+#endif
                     uint32_t f = ((A >= lo && A <= hi) ? 1u : 0u) | ((m2 >= lo && m2 <= hi) ? 2u : 0u) |
                                  ((m3 >= lo && m3 <= hi) ? 4u : 0u) | ((jd >= lo && jd <= hi) ? 8u : 0u);
                     f &= fmask;
@@ -1047,6 +1063,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
             float4 ra[NQ], rb[NQ];
 #pragma unroll
             for (int q = 0; q < NQ; ++q) ra[q] = pr[q];
+ENTE_UNROLL(ENTE_CNT_UNROLL)
             for (int s = 0; s < PER; s += 2, pr += 2 * STRIDE) {
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) rb[q] = pr[STRIDE + q];
