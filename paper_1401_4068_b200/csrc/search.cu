@@ -34,6 +34,8 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <mutex>
+#include <set>
 #include <vector>
 
 #include "common.cuh"
@@ -862,6 +864,22 @@ static RescanFn rescan_table(int dy, int dx, int k) {
          : k <= 32 ? ss.rescan[3] : ss.rescan[4];
 }
 
+// The one-warp sweep CTAs are resident 32 per SM only with the whole
+// 228 KB shared-memory carve-out (the count pass needs 6.1 KB + 1 KB
+// reserved per CTA); ask for it once per kernel.
+#ifndef ENTE_CARVEOUT
+#define ENTE_CARVEOUT 1
+#endif
+static void prefer_shared(const void *fn) {
+    static std::mutex mu;
+    static std::set<const void *> done;
+    if (!ENTE_CARVEOUT || !fn) return;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.insert(fn).second)
+        cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
+}
+
 static CountFn count_table(int dy, int dx, int max_npad) {
     SweepSet ss;
     if (!find_sweep_set(dy, dx, ss)) return nullptr;
@@ -1265,15 +1283,19 @@ static int search_impl(const double *pts64, int64_t total_rows, int dim, const e
         ENTE_CUDA(cudaMemcpyAsync(w.tile0, htile0.data(), sizeof(int32_t) * (2 * n_chunks + 1),
                                   cudaMemcpyHostToDevice, st));
         const unsigned nt = (unsigned)ntiles;
+        const KnnFn knn_fn = knn_table(p.dy, p.dx, p.slots, p.max_npad);
+        const CountFn count_fn = count_table(p.dy, p.dx, p.max_npad);
+        prefer_shared(reinterpret_cast<const void *>(knn_fn));
+        prefer_shared(reinterpret_cast<const void *>(count_fn));
         ENTE_LAUNCH("knn_pass", st,
-                    knn_table(p.dy, p.dx, p.slots, p.max_npad)<<<nt, 32, 0, st>>>(w.pts32k, w.fboxk, w.info,
+                    knn_fn<<<nt, 32, 0, st>>>(w.pts32k, w.fboxk, w.info,
                                                                      w.tile0, n_chunks, k, prune, w.kmap, w.t32,
                                                                      w.L, work));
         ENTE_CUDA(cudaGetLastError());
         uint32_t fmask = 8u;
         for (int o = 0; o < p.lay.nout; ++o) fmask |= 1u << p.lay.slot[o];
         ENTE_LAUNCH("count_pass", st,
-                    count_table(p.dy, p.dx, p.max_npad)<<<nt, 32, 0, st>>>(w.pts32, w.fbox, w.info, w.tile0, n_chunks,
+                    count_fn<<<nt, 32, 0, st>>>(w.pts32, w.fbox, w.info, w.tile0, n_chunks,
                                                                w.t32, ws_rows, prune, w.cnt3, w.ev,
                                                                w.ev_n, fmask, work + 1));
         ENTE_CUDA(cudaGetLastError());

@@ -322,8 +322,17 @@ __device__ __forceinline__ float point_box(const float2 (&nr)[NP], const Box<Q> 
 template <int DP, int NSLOT>
 struct Ring {
     float buf[NSLOT][kSub * DP];
-    float spill[8 * DP];  // read (never used) by the count pass's last row prefetch
     uint64_t full[NSLOT];
+};
+
+// Shared memory of the compacted sweeps: the ring, then the references.
+// The grouped rounds' last row prefetch reads up to 8 rows past the last
+// ring slot (values never used); they land in `full` and `rs`, which are
+// larger than that, so no padding is needed.
+template <class RingT, class RefsT>
+struct __align__(128) SweepSmem {
+    RingT ring;
+    RefsT rs;
 };
 
 template <int DP, int NSLOT>
@@ -522,8 +531,9 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) kn
     constexpr int NBC = D < 4 * kKnnQ ? D : 4 * kKnnQ;  // box columns 0 .. NBC-1
     constexpr int GC = 2 * PG < D ? 2 * PG : D;          // gate columns 0 .. GC-1
     constexpr int NQ = DP / 4;
-    __shared__ __align__(128) Ring<DP, NSLOT> ring;
-    __shared__ __align__(16) KnnRefs<DP, S> rs;
+    __shared__ SweepSmem<Ring<DP, NSLOT>, KnnRefs<DP, S>> sm;
+    auto &ring = sm.ring;
+    auto &rs = sm.rs;
     const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
@@ -657,7 +667,7 @@ ENTE_UNROLL(ENTE_KNNC_UNROLL)
                 for (int q = 0; q < NQ; ++q) rb[q] = pr[STRIDE + q];
                 visit(ra);
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) ra[q] = pr[2 * STRIDE + q];  // may read Ring::spill
+                for (int q = 0; q < NQ; ++q) ra[q] = pr[2 * STRIDE + q];  // may read past the ring (SweepSmem)
                 visit(rb);
             }
             // merge the groups' lists into group 0 (tree; lists are ascending)
@@ -890,7 +900,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
 template <int DP, int NSLOT>
 struct CountRefs {
     float ref[32 * kRT][DP];  // fp32 centred coordinates
-    float lo[32 * kRT], hi[32 * kRT], t[32 * kRT], w[32 * kRT];
+    float lo[32 * kRT], hi[32 * kRT], w[32 * kRT];
     uint32_t cnt[3][32 * kRT];
     int nev[32 * kRT];
     int slot[32 * kRT];       // compacted reference list of the current sub-tile
@@ -906,8 +916,9 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
     using L = Lay<DY, DX>;
     constexpr int D = L::D, DP = L::DP, NP = L::NP, PG = L::PG;
     constexpr int NSLOT = L::NSLOT < ENTE_CNT_NSLOT ? L::NSLOT : ENTE_CNT_NSLOT;
-    __shared__ __align__(128) Ring<DP, NSLOT> ring;
-    __shared__ __align__(16) CountRefs<DP, NSLOT> rs;
+    __shared__ SweepSmem<Ring<DP, NSLOT>, CountRefs<DP, NSLOT>> sm;
+    auto &ring = sm.ring;
+    auto &rs = sm.rs;
     const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
@@ -936,7 +947,6 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
         }
         rs.lo[ri] = b.lo;
         rs.hi[ri] = b.hi;
-        rs.t[ri] = b.nt;
         rs.w[ri] = b.w;
         myhi[r] = b.hi;
         rs.cnt[0][ri] = rs.cnt[1][ri] = rs.cnt[2][ri] = 0u;
@@ -1068,7 +1078,7 @@ ENTE_UNROLL(ENTE_CNT_UNROLL)
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) rb[q] = pr[STRIDE + q];
                 visit(ra, s * G + g);
-                // the last iteration reads G rows past the slot (Ring::spill)
+                // the last iteration may read G rows past the ring (SweepSmem)
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) ra[q] = pr[2 * STRIDE + q];
                 visit(rb, (s + 1) * G + g);
