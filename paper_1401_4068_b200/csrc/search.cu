@@ -369,9 +369,12 @@ __global__ void __launch_bounds__(T) sort_pca_kernel(
             z1 += cs->axis[1][c] * x;
         }
     };
+    // one pass over the fp64 rows: projections parked in the key buffers
     for (int i = threadIdx.x; i < ci.n; i += T) {
         float z0, z1;
         proj(i, z0, z1);
+        k0[i] = __float_as_uint(z0);
+        k1[i] = __float_as_uint(z1);
         mn0 = fminf(mn0, z0);
         mx0 = fmaxf(mx0, z0);
         mn1 = fminf(mn1, z1);
@@ -400,9 +403,8 @@ __global__ void __launch_bounds__(T) sort_pca_kernel(
     const float q = 4095.0f;  // 12 bits per axis: 24-bit keys, three radix passes
     const float s0 = mx0 > mn0 ? q / (mx0 - mn0) : 0.0f;
     const float s1 = mx1 > mn1 ? q / (mx1 - mn1) : 0.0f;
-    for (int i = threadIdx.x; i < ci.n; i += T) {
-        float z0, z1;
-        proj(i, z0, z1);
+    for (int i = threadIdx.x; i < ci.n; i += T) {  // same thread, same i: no barrier needed
+        const float z0 = __uint_as_float(k0[i]), z1 = __uint_as_float(k1[i]);
         const uint32_t a = (uint32_t)fminf(fmaxf((z0 - mn0) * s0, 0.0f), q);
         const uint32_t b = (uint32_t)fminf(fmaxf((z1 - mn1) * s1, 0.0f), q);
         k0[i] = (spread15(a) << 1) | spread15(b);
