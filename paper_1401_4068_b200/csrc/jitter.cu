@@ -67,27 +67,71 @@ struct JitChunk {
     U128 state, inc;
 };
 
-// one warp per chunk, one lane per column: numpy's sequential axis-0 sums
+// One warp per chunk: numpy's sequential axis-0 sums, one lane per column.
+// Blocks of 32 rows are loaded coalesced (lane l takes elements l, l + 32,
+// ... of the block) into shared memory, the next block's loads overlapping
+// this block's dependent fp64 additions; the column lanes then add the
+// block's rows in row order, exactly as numpy does.
+template <int DM>
 __global__ void __launch_bounds__(32) jitter_std_kernel(const double *__restrict__ pts, int dim,
                                                         const JitChunk *__restrict__ ch,
                                                         double amplitude,
                                                         double *__restrict__ half_width) {
+    __shared__ double buf[32 * DM];
     const JitChunk c = ch[blockIdx.x];
-    const int col = threadIdx.x;
-    if (col >= dim) return;
-    const double *p = pts + c.row0 * dim + col;
-    double s = 0.0;
-#pragma unroll 32
-    for (int r = 0; r < c.n; ++r) s = __dadd_rn(s, p[(int64_t)r * dim]);
-    const double mean = __ddiv_rn(s, (double)c.n);
-    double v = 0.0;
-#pragma unroll 32
-    for (int r = 0; r < c.n; ++r) {
-        const double d = __dsub_rn(p[(int64_t)r * dim], mean);
-        v = __dadd_rn(v, __dmul_rn(d, d));
+    const int lane = threadIdx.x;
+    const double *p = pts + c.row0 * dim;
+    const int64_t total = (int64_t)c.n * dim;
+    const int per = 32 * dim;  // elements per 32-row block
+    const int nblk = (c.n + 31) / 32;
+    double reg[DM];
+    auto load = [&](int b) {
+        const int64_t e0 = (int64_t)b * per + lane;
+#pragma unroll
+        for (int i = 0; i < DM; ++i) {
+            const int64_t e = e0 + 32 * i;
+            reg[i] = (i < dim && e < total) ? p[e] : 0.0;
+        }
+    };
+    auto stash = [&]() {
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < DM; ++i)
+            if (i < dim) buf[32 * i + lane] = reg[i];
+        __syncwarp();
+    };
+    // pass 1: sequential sum -> mean
+    double sum = 0.0;
+    load(0);
+    for (int b = 0; b < nblk; ++b) {
+        stash();
+        if (b + 1 < nblk) load(b + 1);
+        const int rows = min(32, c.n - 32 * b);
+        if (lane < dim) {
+#pragma unroll 8
+            for (int r = 0; r < rows; ++r) sum = __dadd_rn(sum, buf[r * dim + lane]);
+        }
     }
-    const double sd = __dsqrt_rn(__ddiv_rn(v, (double)c.n));
-    half_width[(int64_t)blockIdx.x * kMaxDim + col] = __dmul_rn(amplitude, sd);
+    const double mean = __ddiv_rn(sum, (double)c.n);
+    // pass 2: sequential sum of squared deviations
+    double v = 0.0;
+    load(0);
+    for (int b = 0; b < nblk; ++b) {
+        stash();
+        if (b + 1 < nblk) load(b + 1);
+        const int rows = min(32, c.n - 32 * b);
+        if (lane < dim) {
+#pragma unroll 8
+            for (int r = 0; r < rows; ++r) {
+                const double d = __dsub_rn(buf[r * dim + lane], mean);
+                v = __dadd_rn(v, __dmul_rn(d, d));
+            }
+        }
+    }
+    if (lane < dim) {
+        const double sd = __dsqrt_rn(__ddiv_rn(v, (double)c.n));
+        half_width[(int64_t)blockIdx.x * kMaxDim + lane] = __dmul_rn(amplitude, sd);
+    }
 }
 
 // Element e of a chunk (C order) takes the PCG64 output after step e + 1.
@@ -261,8 +305,12 @@ extern "C" int ente_jitter(double *pts64, int dim, const ente_chunk *chunks, int
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ENTE_CUDA(cudaMemcpyAsync(w.ch, h.data(), sizeof(JitChunk) * n_chunks, cudaMemcpyHostToDevice, st));
     if (amplitude > 0) {
-        ENTE_LAUNCH("jitter_std", st,
-                    jitter_std_kernel<<<n_chunks, 32, 0, st>>>(pts64, dim, w.ch, amplitude, w.hw));
+        if (dim <= 8)
+            ENTE_LAUNCH("jitter_std", st,
+                        jitter_std_kernel<8><<<n_chunks, 32, 0, st>>>(pts64, dim, w.ch, amplitude, w.hw));
+        else
+            ENTE_LAUNCH("jitter_std", st,
+                        jitter_std_kernel<kMaxDim><<<n_chunks, 32, 0, st>>>(pts64, dim, w.ch, amplitude, w.hw));
         ENTE_CUDA(cudaGetLastError());
         // small chunks: 64 threads, so the per-thread jump-ahead set-up is
         // amortised over more elements
