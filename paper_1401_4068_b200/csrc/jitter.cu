@@ -168,12 +168,16 @@ __global__ void __launch_bounds__(kJitThreads) jitter_apply_kernel(double *__res
         U128 s = pcg_advance(c.state, c.inc, (uint64_t)e + 1);  // state after step e + 1
         double *p = pts + c.row0 * dim;
         const double *hw = half_width + (int64_t)ci * kMaxDim;
+        int col = (int)(e % dim);            // column of element e, stepped without division
+        const int dcol = kJitThreads % dim;
         for (int i = 0; i < kJitPerThread && e < total; ++i, e += kJitThreads) {
             const uint64_t raw = pcg_output(s);
             const double u01 = (double)(raw >> 11) * 0x1p-53;
             const double u = __dadd_rn(-1.0, 2.0 * u01);
-            p[e] = __dadd_rn(p[e], __dmul_rn(u, hw[(int)(e % dim)]));
+            p[e] = __dadd_rn(p[e], __dmul_rn(u, hw[col]));
             s = add128(mul128(A, s), C);
+            col += dcol;
+            if (col >= dim) col -= dim;
         }
     }
 }
