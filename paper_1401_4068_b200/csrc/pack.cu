@@ -26,25 +26,38 @@ struct PackItem {
     int32_t pad_;
 };
 
-__global__ void __launch_bounds__(256) pack_te_kernel(
+// One thread per output row gathers it into shared memory; the CTA's rows
+// (contiguous in the output) are then written back with coalesced stores.
+constexpr int kPackThreads = 256;
+
+__global__ void __launch_bounds__(kPackThreads) pack_te_kernel(
     const double *__restrict__ x, const double *__restrict__ y, int reps, int n_samples, int dx,
     int tau_x, int dy, int tau_y, int w, const PackItem *__restrict__ items, int n_items,
     const int32_t *__restrict__ perms, double *__restrict__ out) {
+    extern __shared__ double stage[];  // [kPackThreads * dim]
     const int64_t rows = (int64_t)reps * w;
-    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (row >= rows) return;
-    const int r = (int)(row / w);
+    const int64_t row0 = (int64_t)blockIdx.x * kPackThreads;
+    const int64_t row = row0 + threadIdx.x;
+    const bool valid = row < rows;
+    const int r = valid ? (int)(row / w) : 0;
     const int dim = 1 + dy + dx;
+    const int nrow = (int)(rows - row0 < kPackThreads ? rows - row0 : kPackThreads);
     for (int item = blockIdx.y; item < n_items; item += gridDim.y) {  // grid.y <= 65535
         const PackItem it = items[item];
-        const int tp = it.t_lo + (int)(row - (int64_t)r * w);  // 1-based t'
-        const int ry = it.perm >= 0 ? perms[(int64_t)it.perm * reps + r] : r;
-        double *o = out + ((int64_t)item * rows + row) * dim;
-        const double *yr = y + (int64_t)ry * n_samples;
-        const double *xr = x + (int64_t)r * n_samples;
-        o[0] = yr[tp - 1];
-        for (int j = 0; j < dy; ++j) o[1 + j] = yr[tp - 2 - j * tau_y];
-        for (int j = 0; j < dx; ++j) o[1 + dy + j] = xr[tp - 1 - it.u - j * tau_x];
+        if (valid) {
+            const int tp = it.t_lo + (int)(row - (int64_t)r * w);  // 1-based t'
+            const int ry = it.perm >= 0 ? perms[(int64_t)it.perm * reps + r] : r;
+            double *o = stage + threadIdx.x * dim;
+            const double *yr = y + (int64_t)ry * n_samples;
+            const double *xr = x + (int64_t)r * n_samples;
+            o[0] = yr[tp - 1];
+            for (int j = 0; j < dy; ++j) o[1 + j] = yr[tp - 2 - j * tau_y];
+            for (int j = 0; j < dx; ++j) o[1 + dy + j] = xr[tp - 1 - it.u - j * tau_x];
+        }
+        __syncthreads();
+        double *dst = out + ((int64_t)item * rows + row0) * dim;
+        for (int e = threadIdx.x; e < nrow * dim; e += kPackThreads) dst[e] = stage[e];
+        __syncthreads();
     }
 }
 
@@ -113,10 +126,17 @@ extern "C" int ente_pack_te_items(const double *x, const double *y, int reps, in
     }
     ENTE_CUDA(cudaMemcpyAsync(ditems, h.data(), sizeof(PackItem) * n_items, cudaMemcpyHostToDevice, st));
     const int64_t rows = (int64_t)reps * w;
-    dim3 grid((unsigned)((rows + 255) / 256), (unsigned)(n_items < 65535 ? n_items : 65535));
+    dim3 grid((unsigned)((rows + kPackThreads - 1) / kPackThreads),
+              (unsigned)(n_items < 65535 ? n_items : 65535));
+    const size_t smem = sizeof(double) * kPackThreads * (size_t)(1 + dx + dy);  // <= 64 KB
+    static std::once_flag smem_once;
+    std::call_once(smem_once, [] {
+        cudaFuncSetAttribute(pack_te_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * kPackThreads * kMaxDim));
+    });
     ENTE_LAUNCH("pack_te", st,
-                pack_te_kernel<<<grid, 256, 0, st>>>(x, y, reps, n_samples, dx, tau_x, dy, tau_y, w,
-                                                     ditems, n_items, perms, out));
+                pack_te_kernel<<<grid, kPackThreads, smem, st>>>(x, y, reps, n_samples, dx, tau_x, dy,
+                                                                 tau_y, w, ditems, n_items, perms, out));
     ENTE_CUDA(cudaGetLastError());
     // (a pageable-source cudaMemcpyAsync has staged h before returning)
     return ENTE_OK;
