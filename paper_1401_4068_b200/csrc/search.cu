@@ -842,9 +842,14 @@ __global__ void __launch_bounds__(kIdxWarps * 32) knn_index_kernel(
 // ---------------------------------------------------------------------------
 // Layout tables: the sweeps of every compiled (d_y, d_x) live in the
 // sweeps_*.cu translation units (sweeps.cuh).
-// Chunks of a few sub-tiles: nearly every reference needs every sub-tile,
-// so compaction only adds its overhead; the direct two-per-lane sweeps win.
-constexpr int kCompactMinRows = 4096;
+// Smallest chunk (padded rows of the batch's largest) for the compacted
+// sweeps.  With grouped rounds they win even on 500-row chunks (C4: count
+// pass 40.2 -> 31.2 ms), so the direct two-refs-per-lane sweeps are kept
+// only for -DENTE_COMPACT_MIN_ROWS=<n> builds and k + 1 > 16.
+#ifndef ENTE_COMPACT_MIN_ROWS
+#define ENTE_COMPACT_MIN_ROWS 0
+#endif
+constexpr int kCompactMinRows = ENTE_COMPACT_MIN_ROWS;
 
 #ifndef ENTE_KNN_COMPACT
 #define ENTE_KNN_COMPACT 1
