@@ -17,8 +17,8 @@
 namespace ente {
 
 constexpr int kSortThreads = 512;      // CTA size for large segments
-constexpr int kSortThreadsSmall = 128;  // ... for segments of <= kSortSmallN keys
-constexpr int kSortSmallN = 2048;
+constexpr int kSortThreadsSmall = 128;  // ... for segments of <= kSortSmallN keys,
+constexpr int kSortSmallN = 1024;       // sorted in shared memory (keys + values: 16 KB)
 constexpr int kSortItems = 8;  // keys per thread per tile
 
 template <int T>

@@ -305,8 +305,12 @@ __global__ void __launch_bounds__(T) sort_kernel(
     }
     __syncthreads();
     const double *p = pts64 + ci.row0 * dim;
-    uint32_t *k0 = ka + ci.row0, *k1 = kb + ci.row0;
-    int32_t *v0 = va + ci.row0, *v1 = vb + ci.row0;
+    // small segments (the 128-thread instantiation) sort in shared memory
+    constexpr bool SMS = T == kSortThreadsSmall;
+    __shared__ uint32_t skey[SMS ? 2 : 1][SMS ? kSortSmallN : 1];
+    __shared__ int32_t sval[SMS ? 2 : 1][SMS ? kSortSmallN : 1];
+    uint32_t *k0 = SMS ? skey[0] : ka + ci.row0, *k1 = SMS ? skey[1] : kb + ci.row0;
+    int32_t *v0 = SMS ? sval[0] : va + ci.row0, *v1 = SMS ? sval[1] : vb + ci.row0;
     for (int i = threadIdx.x; i < ci.n; i += T) {
         uint32_t key = 0;
         uint32_t q[kMaxDim];
@@ -357,8 +361,11 @@ __global__ void __launch_bounds__(T) sort_pca_kernel(
     }
     const int P = dim < kPcaCols ? dim : kPcaCols;
     const double *p = pts64 + ci.row0 * dim;
-    uint32_t *k0 = ka + ci.row0, *k1 = kb + ci.row0;
-    int32_t *v0 = va + ci.row0, *v1 = vb + ci.row0;
+    constexpr bool SMS = T == kSortThreadsSmall;  // small segments sort in shared memory
+    __shared__ uint32_t skey[SMS ? 2 : 1][SMS ? kSortSmallN : 1];
+    __shared__ int32_t sval[SMS ? 2 : 1][SMS ? kSortSmallN : 1];
+    uint32_t *k0 = SMS ? skey[0] : ka + ci.row0, *k1 = SMS ? skey[1] : kb + ci.row0;
+    int32_t *v0 = SMS ? sval[0] : va + ci.row0, *v1 = SMS ? sval[1] : vb + ci.row0;
     float mn0 = INFINITY, mx0 = -INFINITY, mn1 = INFINITY, mx1 = -INFINITY;
     auto proj = [&](int i, float &z0, float &z1) {
         z0 = 0.0f;

@@ -145,8 +145,10 @@ __global__ void __launch_bounds__(T) te_reduce_kernel(
     __shared__ int n_leaves;
     const RedChunk ch = chunks[blockIdx.x];
     const int n = ch.n;
-    uint64_t *src = ka + ch.row0;
-    uint64_t *dst = kb + ch.row0;
+    constexpr bool SMS = T == kSortThreadsSmall;  // small segments sort in shared memory
+    __shared__ uint64_t skey[SMS ? 2 : 1][SMS ? kSortSmallN : 1];
+    uint64_t *src = SMS ? skey[0] : ka + ch.row0;
+    uint64_t *dst = SMS ? skey[1] : kb + ch.row0;
     if (threadIdx.x == 0) bad = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += T) {
