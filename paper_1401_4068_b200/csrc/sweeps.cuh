@@ -182,8 +182,8 @@ __device__ __forceinline__ float warp_max_nonneg(float v) {
 // ---------------------------------------------------------------------------
 // Warp-private candidate stream.
 //
-// Each sweep CTA is ONE warp owning 128 consecutive sorted references (4 per
-// lane).  It walks the chunk's 32-row sub-tiles home-first, then alternately
+// Each sweep CTA is ONE warp owning 32 * kRT (64) consecutive sorted
+// references (kRT per lane).  It walks the chunk's 32-row sub-tiles home-first, then alternately
 // below and above (nearest first in the Morton order, so kNN bounds shrink
 // early).  Sub-tile boxes are tested 32 positions at a time, one per lane,
 // with the next window's boxes prefetched into registers; needed sub-tiles
