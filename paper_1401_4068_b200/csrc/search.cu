@@ -125,6 +125,7 @@ constexpr int kPrepThreadsBig = 256;   // CTA size for chunks of > kPrepSmallN r
 constexpr int kPrepThreadsSmall = 64;  // ... and for small chunks (C4: 500 rows)
 constexpr int kPrepSmallN = 2048;
 constexpr int kCovN = kPcaCols * (kPcaCols + 1) / 2;
+constexpr int kCovStride = 4;  // covariance from rows 0, 4, 8, ...
 
 template <int kPrepThreads>
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double *__restrict__ pts64, int dim,
@@ -166,15 +167,17 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double *__rest
                 nonfinite |= !isfinite(v[i]);
             }
         }
-        // second sweep over the (L2-resident) rows for the covariance, kept
-        // apart so that neither loop needs more than ~64 registers
+        // second sweep for the covariance, kept apart so that neither loop
+        // needs more than ~64 registers.  The axes only choose the kNN order
+        // (never a result), so every kCovStride-th row suffices (the chunks
+        // are not L2-resident); the sums are rescaled to n rows below.
         float cov[kCovN], x0[kPcaCols];
 #pragma unroll
         for (int e = 0; e < kCovN; ++e) cov[e] = 0.0f;
 #pragma unroll
         for (int i = 0; i < kPcaCols; ++i) x0[i] = (g0 == 0 && i < P) ? (float)p[i] : 0.0f;
         if (g0 == 0 && stats && ci.n >= kPcaMinRows) {
-            for (int r = threadIdx.x; r < ci.n; r += kPrepThreads) {
+            for (int r = threadIdx.x * kCovStride; r < ci.n; r += kPrepThreads * kCovStride) {
                 float x[kPcaCols];
 #pragma unroll
                 for (int i = 0; i < kPcaCols; ++i) x[i] = i < P ? (float)p[(int64_t)r * dim + i] - x0[i] : 0.0f;
@@ -236,7 +239,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double *__rest
         for (int e = threadIdx.x; e < kCovN; e += blockDim.x) {
             float v = 0.0f;
             for (int w = 0; w < kPrepWarps; ++w) v += wcov[w][e];
-            stats[c].cov[e] = v;
+            stats[c].cov[e] = v * ((float)ci.n / (float)((ci.n + kCovStride - 1) / kCovStride));
         }
         if (threadIdx.x < kPcaCols) stats[c].x0[threadIdx.x] = threadIdx.x < P ? (float)p[threadIdx.x] : 0.0f;
     }
