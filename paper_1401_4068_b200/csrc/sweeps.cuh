@@ -630,6 +630,8 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) kn
         auto run_round = [&](auto lgc, int round) {
             constexpr int LG = decltype(lgc)::value;
             constexpr int G = 1 << LG, PER = 32 >> LG, STRIDE = G * NQ;
+            constexpr int STEPS = kSub >> LG;  // candidate rows per lane (even: kSub >= 16, G <= 8)
+            static_assert(STEPS >= 2 && STEPS % 2 == 0, "row pairs");
             const int g = lane >> (5 - LG);
             const int it = lane & (PER - 1);
             const bool active = round + it < nneed;
@@ -662,7 +664,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) kn
 #pragma unroll
             for (int q = 0; q < NQ; ++q) ra[q] = pr[q];
 ENTE_UNROLL(ENTE_KNNC_UNROLL)
-            for (int s = 0; s < PER; s += 2, pr += 2 * STRIDE) {
+            for (int s = 0; s < STEPS; s += 2, pr += 2 * STRIDE) {
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) rb[q] = pr[STRIDE + q];
                 visit(ra);
@@ -1018,6 +1020,8 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
         auto run_round = [&](auto lgc, int round) {
             constexpr int LG = decltype(lgc)::value;
             constexpr int G = 1 << LG, PER = 32 >> LG, STRIDE = G * NQ;
+            constexpr int STEPS = kSub >> LG;  // candidate rows per lane (even: kSub >= 16, G <= 8)
+            static_assert(STEPS >= 2 && STEPS % 2 == 0, "row pairs");
             const int g = lane >> (5 - LG);  // group: candidate rows g, g + G, g + 2G, ...
             const int it = lane & (PER - 1);
             const bool active = round + it < nneed;
@@ -1074,7 +1078,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
 #pragma unroll
             for (int q = 0; q < NQ; ++q) ra[q] = pr[q];
 ENTE_UNROLL(ENTE_CNT_UNROLL)
-            for (int s = 0; s < PER; s += 2, pr += 2 * STRIDE) {
+            for (int s = 0; s < STEPS; s += 2, pr += 2 * STRIDE) {
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) rb[q] = pr[STRIDE + q];
                 visit(ra, s * G + g);
