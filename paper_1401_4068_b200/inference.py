@@ -366,12 +366,35 @@ def analyze_windows(source: EnsembleSeries, target: EnsembleSeries, spec_x: Embe
     items[:, :2] = np.tile(per_win, (len(starts), 1))
     items[:, 2] = np.repeat(starts, len(per_win))
     te_all = pipe.run(items).reshape(len(windows), len(per_win))
+    return _assemble_results(source, target, config, windows, us, grid,
+                             te_all[:, :len(us)], te_all[:, len(us):].reshape(len(windows), len(grid), s))
+
+
+def _assemble_results(source, target, config, windows, us, grid, te_orig, te_surr) -> list:
+    """_assemble_result for many windows at once (same values: the per-window
+    statistics of inference.py:153-193 as array operations over windows)."""
+    s = config.n_surrogates
+    te_orig = np.asarray(te_orig, dtype=np.float64)
+    # surrogate statistic: running np.maximum over the grid rows from -inf
+    surrogates = np.full((len(windows), s), -np.inf)
+    for g in range(len(grid)):
+        np.maximum(surrogates, te_surr[:, g, :], out=surrogates)
+    in_grid = [i for i, u in enumerate(us) if u in grid]
+    medians = np.median(surrogates, axis=1)
     results = []
-    for (lo, hi), row in zip(windows, te_all):
-        te_orig = row[:len(us)]
-        te_surr = row[len(us):].reshape(len(grid), s)
-        results.append(_assemble_result(source, target, dataclasses.replace(config, window=(lo, hi)),
-                                        us, grid, te_orig, te_surr))
+    for wi, (lo, hi) in enumerate(windows):
+        curve = [(u, float(t)) for u, t in zip(us, te_orig[wi])]
+        u_best, te_best = max(curve, key=lambda ut: (ut[1], -ut[0]))
+        stat_orig = max(curve[i][1] for i in in_grid)
+        hits = int(np.count_nonzero(surrogates[wi] >= stat_orig))
+        p = (hits + 1) / (s + 1) if config.conservative_pvalue else hits / s
+        sig = p < config.alpha
+        results.append(TEResult(source=source.channel_name, target=target.channel_name,
+                                window=(lo, hi), u_selected=u_best, te_value=te_best,
+                                surrogate_values=surrogates[wi].copy(), p_value=p, significant=sig,
+                                significant_corrected=sig,
+                                te_minus_median_surrogate=te_best - float(medians[wi]),
+                                te_curve=curve))
     return results
 
 
