@@ -165,3 +165,35 @@ def test_workloads_match_reference_simulators(golden):
     for name in ("C1", "C2"):
         x, y = workloads.CONFIGS[name].ensembles()
         assert cases.sha(x, y) == str(g[f"{name.lower()}_sha"])
+
+
+def test_window_statistics_batch_matches_per_window():
+    """analyze_windows' array statistics equal analyze_pair's per-window host
+    statistics (inference.py:153-193), NaN surrogates and both p-value forms."""
+    import dataclasses
+
+    import numpy as np
+
+    from paper_1401_4068_b200.data import AnalysisConfig, EnsembleSeries
+    from paper_1401_4068_b200.inference import _assemble_result, _assemble_results
+
+    rng = np.random.default_rng(5)
+    X = EnsembleSeries("X", rng.standard_normal((4, 60)))
+    Y = EnsembleSeries("Y", rng.standard_normal((4, 60)))
+    for cons in (False, True):
+        cfg = AnalysisConfig(u_candidates=(3, 5, 7), window=(20, 20), k=4, n_surrogates=40,
+                             seed=0, conservative_pvalue=cons, test_grid=(5, 7))
+        us, grid = list(cfg.u_candidates), list(cfg.test_grid)
+        te_o = np.round(rng.random((25, len(us))), 1)           # ties in the delay scan
+        te_s = np.round(rng.random((25, len(grid), 40)), 1)
+        te_s[3, 0, 5] = np.nan
+        windows = [(20 + i, 20 + i) for i in range(25)]
+        one = [_assemble_result(X, Y, dataclasses.replace(cfg, window=w), us, grid, te_o[i], te_s[i])
+               for i, w in enumerate(windows)]
+        batch = _assemble_results(X, Y, cfg, windows, us, grid, te_o, te_s)
+        for a, b in zip(one, batch):
+            da, db = dataclasses.asdict(a), dataclasses.asdict(b)
+            assert np.array_equal(da.pop("surrogate_values"), db.pop("surrogate_values"), equal_nan=True)
+            ma, mb = da.pop("te_minus_median_surrogate"), db.pop("te_minus_median_surrogate")
+            assert ma == mb or (np.isnan(ma) and np.isnan(mb))
+            assert da == db
