@@ -41,9 +41,6 @@ constexpr int kGate = 4;                    // gate columns in the Morton key an
 #endif
 #define ENTE_PRAGMA(x) _Pragma(#x)
 #define ENTE_UNROLL(n) ENTE_PRAGMA(unroll n)
-#ifndef ENTE_CNT_BANDVOTE
-#define ENTE_CNT_BANDVOTE 0  // count pass: band test as a warp vote
-#endif
 #ifndef ENTE_CNT_UNROLL
 #define ENTE_CNT_UNROLL 2    // count pass: row-pair iterations unrolled per loop trip
 #endif
@@ -1043,29 +1040,27 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
             auto visit = [&](const float4 (&cur)[NQ], int j) {
                 const float2 *c = reinterpret_cast<const float2 *>(cur);
                 float a[2 * NP];
-                diff_pairs<D, 0, PG>(ref, c, a);
+                // Straight line: about half of the (reference, row) pairs a
+                // compacted round visits pass the y-past gate A <= hi, so a
+                // warp vote on it almost never skips a row; all the columns
+                // are differenced unconditionally.  jd = max(m2, m3) is one
+                // of m2, m3, so the band test needs only A, m2, m3.
+                diff_pairs<D, 0, NP>(ref, c, a);
                 const float A = maxabs0<1, 1 + DY, 2 * NP>(a);
-                if (!__any_sync(0xffffffffu, A <= hi)) return;
-                diff_pairs<D, PG, NP>(ref, c, a);
                 const float m2 = fmaxf(A, fabsf(a[0]));
                 const float m3 = maxabs<1 + DY, D, 2 * NP>(a, A);
-                const float jd = fmaxf(m2, m3);
                 const float2 e = __fadd2_rn(make_float2(A, m2), make_float2(nlo, nlo));
-                const float2 e34 = __fadd2_rn(make_float2(m3, jd), make_float2(nlo, nlo));
+                const float e3 = __fadd_rn(m3, nlo);
                 cA += __float_as_uint(e.x) >> 31;
                 c2 += __float_as_uint(e.y) >> 31;
-                c3 += __float_as_uint(e34.x) >> 31;
-                // conservative band test on the same differences: min |v - lo| <= w
-                const float bm = fminf(fminf(fabsf(e.x), fabsf(e.y)), fminf(fabsf(e34.x), fabsf(e34.y)));
-#if ENTE_CNT_BANDVOTE
-                if (__any_sync(0xffffffffu, bm <= wb)) {  // warp-uniform: no reconvergence stack
-#else
+                c3 += __float_as_uint(e3) >> 31;
+                const float bm = fminf(fminf(fabsf(e.x), fabsf(e.y)), fabsf(e3));
                 if (bm <= wb) {
-#endif
+                    const float jd = fmaxf(m2, m3);
                     uint32_t f = ((A >= lo && A <= hi) ? 1u : 0u) | ((m2 >= lo && m2 <= hi) ? 2u : 0u) |
                                  ((m3 >= lo && m3 <= hi) ? 4u : 0u) | ((jd >= lo && jd <= hi) ? 8u : 0u);
                     f &= fmask;
-                    if (f) {  // rare; the groups of one round share references
+                    if (f) {
                         const int pos = atomicAdd(&rs.nev[ri], 1);
                         if (pos < kCap)
                             ev[(ci.row0 + wrow + ri) * kCap + pos] = (uint32_t)(cur_st * kSub + j) | (f << 28);
