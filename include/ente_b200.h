@@ -226,6 +226,32 @@ int ente_te_reduce(const int32_t *counts, int64_t total_rows, const ente_chunk *
                    double *out_te, void *workspace, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * Random streams of the surrogate test (host code, no device work).
+ *
+ * ente_seed_states -- PCG64 state of np.random.default_rng(SeedSequence(e))
+ * for n_items entropy word lists e_i = words[offsets[i] .. offsets[i+1])
+ * (numpy's uint32 coercion of the seed, e.g. (seed, u, idx + 1) -> 3 words):
+ * out [host] n_items x 4 uint64 {state_hi, state_lo, inc_hi, inc_lo}, the
+ * pcg_state layout of ente_jitter.
+ *
+ * Replaces: np.random.default_rng(SeedSequence((seed, u, 0|idx+1)))
+ *           inference.py:148,171-172 -> ksg.py:55
+ *
+ * ente_draw_permutations -- per entropy list i, the permutation of range(reps)
+ * drawn by np.random.default_rng(SeedSequence(e_i)).permutation(reps),
+ * redrawn from the same generator while strict and some phi(r) == r:
+ * out [host] n_perms x reps int32.  strict with reps < 2 is ENTE_ERR_ARG
+ * (InvalidPermutation in the reference).
+ *
+ * Replaces: ente.inference.draw_permutation   inference.py:41-49
+ *           ente.inference._surrogate_seed    inference.py:101-102
+ * ------------------------------------------------------------------------- */
+int ente_seed_states(const uint32_t *words, const int64_t *offsets, int64_t n_items,
+                     uint64_t *out);
+int ente_draw_permutations(const uint32_t *words, const int64_t *offsets, int64_t n_perms,
+                           int reps, int strict, int32_t *out);
+
+/* ---------------------------------------------------------------------------
  * Instrumentation (no reference counterpart: the reference only has
  * time.perf_counter around whole calls, bench.py:71-81).
  *

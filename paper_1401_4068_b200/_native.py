@@ -65,6 +65,8 @@ def _declare(L):
                               i32),
         "ente_microbench_pce": ([i32, i32, ctypes.POINTER(dbl), vp], i32),
         "ente_search_work": ([ctypes.POINTER(ctypes.c_ulonglong)] * 2, None),
+        "ente_seed_states": ([u32p, ctypes.POINTER(i64), i64, u64p], i32),
+        "ente_draw_permutations": ([u32p, ctypes.POINTER(i64), i64, i32, i32, i32p], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
