@@ -271,8 +271,9 @@ int ente_profile_read(char *names, size_t names_len, int64_t *launches, double *
                       int max_kernels);
 int ente_microbench_pce(int iters, int blocks, double *pce_per_s, void *stream);
 /* (reference, candidate) pairs the two sweeps evaluated on the current device
- * since the last call -- whole 32-candidate sub-tiles against a warp's
- * reference group; pruning skips the rest; synchronises */
+ * since the last call: each (reference, 32-row sub-tile) visit counts 32
+ * pairs (lane-level work; pruning skips the rest, idle lanes of partial
+ * rounds are not counted); synchronises */
 void ente_search_work(unsigned long long *knn_pairs, unsigned long long *count_pairs);
 
 #ifdef __cplusplus

@@ -1372,16 +1372,19 @@ extern "C" int ente_search_split(const double *pts64, int64_t total_rows, int di
                        out_counts, status, workspace, ws_bytes, stream, split_index, split_count);
 }
 
-// Evaluated (reference, candidate) pairs (whole sub-tiles x reference groups) of the two sweeps on the
-// current device since the last call (synchronises the device): the pruned
-// work actually done.
+// Evaluated (reference, candidate) pairs of the two sweeps on the current
+// device since the last call (synchronises the device): every (reference,
+// sub-tile) visit the sweeps made -- compacted references of a sub-tile, or
+// every reference of the warp in the direct variants -- times the sub-tile's
+// rows.  This is the lane-level work; lanes left idle by partial rounds are
+// not counted.
 extern "C" void ente_search_work(unsigned long long *knn_pairs, unsigned long long *count_pairs) {
     unsigned long long h[2] = {0, 0};
     unsigned long long *d = device_work();
     if (d && cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess)
         cudaMemset(d, 0, sizeof(h));
-    *knn_pairs = h[0] * (unsigned long long)(kSub * kWarpRefs);
-    *count_pairs = h[1] * (unsigned long long)(kSub * kWarpRefs);
+    *knn_pairs = h[0] * (unsigned long long)kSub;
+    *count_pairs = h[1] * (unsigned long long)kSub;
 }
 
 

@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(32, S > 16 ? 24 : (S > 8 ? 16 : sweep_minb(1 +
                 }
             }
         }
-        ++nsub;
+        nsub += kWarpRefs;  // every reference of the warp visits the sub-tile
         float wb = 0.0f;
 #pragma unroll
         for (int r = 0; r < kRT; ++r) wb = fmaxf(wb, kd[r][SR - 1]);
@@ -699,7 +699,7 @@ ENTE_UNROLL(ENTE_KNNC_UNROLL)
             else
                 run_round(std::integral_constant<int, 0>{}, round);
         }
-        ++nsub;
+        nsub += nneed;  // (reference, sub-tile) visits of compacted references
         bound = warp_bound();
         const int st = wk.next(fb, prune ? bound : INFINITY, true, refs_need);
         if (st >= 0) {
@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
                 }
             }
         }
-        ++nsub;
+        nsub += kWarpRefs;  // every reference of the warp visits the sub-tile
         __syncwarp();
         const int st = wk.next(fb, prune ? bound : INFINITY, false, refs_need);
         if (st >= 0) {
@@ -1107,7 +1107,7 @@ ENTE_UNROLL(ENTE_CNT_UNROLL)
             else
                 run_round(std::integral_constant<int, 0>{}, round);
         }
-        ++nsub;
+        nsub += nneed;  // (reference, sub-tile) visits of compacted references
         __syncwarp();
         const int st = wk.next(fb, prune ? bound : INFINITY, false, refs_need);
         if (st >= 0) {

@@ -23,6 +23,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
+from . import seeds
 from .data import AnalysisConfig, EnsembleSeries, TEResult, validate_ensemble
 from .embedding import EmbeddingSpec, PointSetBundle, check_assembly
 from .exceptions import EnteError, InvalidPermutation, KTooLarge, UnknownMethod
@@ -111,32 +112,27 @@ def _permuted_bundle(bundle: PointSetBundle, permutation: np.ndarray,
 
 
 # ---------------------------------------------------------------------------
-# host prep caches (pure functions of their keys)
+# random streams: native batch derivation (csrc/seeds.cu), bit-equal to numpy
 # ---------------------------------------------------------------------------
-_PERMS: dict = {}
-_STATES: dict = {}
-_MASK64 = (1 << 64) - 1
+def surrogate_perms(master_seed, count: int, reps: int, strict: bool) -> np.ndarray:
+    """The S = count surrogate permutations of analyze_pair, [count, reps] int32:
+    draw_permutation(reps, SeedSequence((master_seed, i)), strict) for i < count
+    (inference.py:101-102, 161-164), drawn natively in one call."""
+    if strict and reps < 2 and count > 0:
+        raise InvalidPermutation("strict permutation needs R >= 2")
+    return seeds.surrogate_permutations(master_seed, count, reps, strict)
 
 
 def cached_permutation(master_seed, idx: int, reps: int, strict: bool) -> np.ndarray:
-    key = (master_seed, idx, reps, strict)
-    perm = _PERMS.get(key)
-    if perm is None:
-        perm = draw_permutation(reps, _surrogate_seed(master_seed, idx), strict).permutation
-        if len(_PERMS) < 1 << 20:
-            _PERMS[key] = perm
-    return perm
+    """Surrogate permutation idx alone (int64, as draw_permutation returns it)."""
+    if strict and reps < 2:
+        raise InvalidPermutation("strict permutation needs R >= 2")
+    return seeds.surrogate_permutations_at(master_seed, [idx], reps, strict)[0].astype(np.int64)
 
 
 def jitter_state(seed_tuple) -> tuple:
     """PCG64 (state, inc) of default_rng(SeedSequence(seed_tuple)) as 4 uint64."""
-    st = _STATES.get(seed_tuple)
-    if st is None:
-        s = np.random.PCG64(np.random.SeedSequence(seed_tuple)).state["state"]
-        st = (s["state"] >> 64, s["state"] & _MASK64, s["inc"] >> 64, s["inc"] & _MASK64)
-        if len(_STATES) < 1 << 22:
-            _STATES[seed_tuple] = st
-    return st
+    return tuple(int(v) for v in seeds.pcg_states([np.random.SeedSequence(seed_tuple)])[0])
 
 
 class PairPipeline:
@@ -168,7 +164,7 @@ class PairPipeline:
         self.perm_count = 0
 
     def set_perms(self, perms):
-        arr = np.ascontiguousarray(np.stack(perms).astype(np.int32))
+        arr = np.ascontiguousarray(np.asarray(perms, dtype=np.int32).reshape(-1, self.reps))
         self.perm_dev = torch.from_numpy(arr).to(nat.device())
         self.perm_count = len(perms)
 
@@ -187,30 +183,39 @@ class PairPipeline:
         return np.ascontiguousarray(it.astype(np.int32))
 
     def run(self, items) -> np.ndarray:
+        te, st = self.run_status(items)
+        if (st != 0).any():
+            _raise_status(int(st[np.flatnonzero(st)[0]]))
+        return te
+
+    def run_status(self, items):
+        """TE values and per-item chunk status codes (0 = ok, else the
+        ente_chunk_status the reference would raise for that item); raises
+        only for errors common to every item (KTooLarge: m <= k)."""
         if len(items) == 0:
-            return np.empty(0)
+            return np.empty(0), np.zeros(0, dtype=np.int32)
         if self.m <= self.cfg.k:
             raise KTooLarge(f"need more than k={self.cfg.k} pooled points, got {self.m}")
         it = self._items(items)
         per_wave = max(1, MAX_ROWS_PER_WAVE // self.m)
-        out = []
+        tes, sts = [], []
         for s in range(0, len(it), per_wave):
-            out.append(self._wave(it[s:s + per_wave]))
-        return np.concatenate(out)
+            te, st = self._wave(it[s:s + per_wave])
+            tes.append(te)
+            sts.append(st)
+        return np.concatenate(tes), np.concatenate(sts).astype(np.int32)
 
     def _states(self, it: np.ndarray) -> np.ndarray:
-        """Jitter PCG64 states per item; seeds depend only on (u, perm), not the window."""
-        key = (it[:, 0].astype(np.int64) << 32) | (it[:, 1].astype(np.int64) + 1)
-        keys, inv = np.unique(key, return_inverse=True)
-        uniq = np.array([jitter_state(self.seed_tuple(int(k >> 32), int(k & 0xFFFFFFFF) - 1))
-                         for k in keys.tolist()], dtype=np.uint64)
-        return np.ascontiguousarray(uniq[inv.reshape(-1)])
+        """Jitter PCG64 states per item: SeedSequence((seed, u, 0 | idx + 1)), independent
+        of the window (inference.py:148, 171-172)."""
+        return np.ascontiguousarray(seeds.jitter_states(self.cfg.seed, it[:, 0],
+                                                        it[:, 1].astype(np.int64) + 1))
 
-    def _wave(self, it: np.ndarray) -> np.ndarray:
+    def _wave(self, it: np.ndarray):
         """One device batch, split into sub-batches alternating over two CUDA
         streams so that one sub-batch's latency-bound kernels (pack, jitter,
         sorts, gathers, reduction) overlap another's compute-bound sweeps.
-        Statuses are read once at the end."""
+        Returns (te, status), read once at the end."""
         n = len(it)
         nsub = 1 if n < 2 * MIN_SUB_BATCH else min(SUB_BATCHES, n // MIN_SUB_BATCH)
         bounds = np.linspace(0, n, nsub + 1).astype(int)
@@ -228,9 +233,7 @@ class PairPipeline:
             main.wait_stream(stream)
         te = torch.cat([t for t, _ in outs]).cpu().numpy()
         st = torch.cat([s for _, s in outs]).cpu().numpy()
-        if (st != 0).any():
-            _raise_status(int(st[np.flatnonzero(st)[0]]))
-        return te
+        return te, st
 
     def _sub(self, it: np.ndarray, states: np.ndarray, tag: str):
         L = nat.lib()
@@ -269,7 +272,9 @@ def analyze_pair(source: EnsembleSeries, target: EnsembleSeries,
     """Delay scan + surrogate test for one directed pair in one window (TE in nats).
 
     x_device / y_device optionally pass the two ensembles already resident in
-    HBM (same values as source / target), skipping their upload.
+    HBM (same values as source / target), skipping their upload.  Errors are
+    raised in the reference's order (inference.py:143-193): the originals of
+    the u values before a failing assembly are estimated first.
     """
     validate_ensemble(source)
     validate_ensemble(target)
@@ -291,9 +296,7 @@ def analyze_pair(source: EnsembleSeries, target: EnsembleSeries,
     originals = [(u, -1) for u in us]
 
     if not selected and assembly_error is None and can_draw:
-        perms = [cached_permutation(config.seed, i, reps, config.strict_permutation)
-                 for i in range(s)]
-        pipe.set_perms(perms)
+        pipe.set_perms(surrogate_perms(config.seed, s, reps, config.strict_permutation))
         surr_items = [(u, i) for u in grid for i in range(s)]
         te_all = pipe.run(originals + surr_items)
         te_orig = te_all[:len(us)]
@@ -302,30 +305,12 @@ def analyze_pair(source: EnsembleSeries, target: EnsembleSeries,
         te_orig = pipe.run(originals)
         if assembly_error is not None:
             raise assembly_error
-        te_surr = None
-    curve = [(u, float(t)) for u, t in zip(us, te_orig)]
-    u_best, te_best = max(curve, key=lambda ut: (ut[1], -ut[0]))
-    if grid is None:
-        grid = (u_best,)
-        stat_orig = te_best
-    else:
-        stat_orig = max(t for u, t in curve if u in grid)
-    if te_surr is None:
-        perms = [cached_permutation(config.seed, i, reps, config.strict_permutation)
-                 for i in range(s)]
-        pipe.set_perms(perms)
+        if grid is None:
+            curve = list(zip(us, te_orig))
+            grid = (max(curve, key=lambda ut: (ut[1], -ut[0]))[0],)
+        pipe.set_perms(surrogate_perms(config.seed, s, reps, config.strict_permutation))
         te_surr = pipe.run([(u, i) for u in grid for i in range(s)]).reshape(len(grid), s)
-    surrogates = np.full(s, -np.inf)
-    for row in te_surr:
-        np.maximum(surrogates, row, out=surrogates)
-    p = permutation_pvalue(stat_orig, surrogates, config.conservative_pvalue)
-    sig = p < config.alpha
-    return TEResult(source=source.channel_name, target=target.channel_name,
-                    window=config.window, u_selected=u_best, te_value=te_best,
-                    surrogate_values=surrogates, p_value=p, significant=sig,
-                    significant_corrected=sig,
-                    te_minus_median_surrogate=te_best - float(np.median(surrogates)),
-                    te_curve=curve)
+    return _assemble_result(source, target, config, us, grid, te_orig, te_surr)
 
 
 def analyze_windows(source: EnsembleSeries, target: EnsembleSeries, spec_x: EmbeddingSpec,
@@ -338,27 +323,35 @@ def analyze_windows(source: EnsembleSeries, target: EnsembleSeries, spec_x: Embe
     jitter streams, exactly as the per-window calls would).  This is the
     non-stationary, TE-per-time-point analysis of the paper: every (window,
     u, surrogate) chunk goes through one pack / jitter / search / reduce
-    sequence.
+    sequence.  Errors surface in the per-window calls' order: the windows
+    before the first failing assembly run first (their own errors win), then
+    the failing window's analyze_pair raises.
     """
-    import dataclasses
-
     validate_ensemble(source)
     validate_ensemble(target)
-    if config.scan_statistic == "selected":
-        return [analyze_pair(source, target, spec_x, spec_y,
-                             dataclasses.replace(config, window=(t, t + _width(config) - 1)))
-                for t in window_starts]
     w = _width(config)
+    windows = [(int(t), int(t) + w - 1) for t in window_starts]
+    if config.scan_statistic == "selected":
+        return [analyze_pair(source, target, spec_x, spec_y, _at_window(config, win))
+                for win in windows]
+    for wi, win in enumerate(windows):
+        try:
+            for u in config.u_candidates:
+                check_assembly(source, target, spec_x, spec_y, u, win)
+        except EnteError:
+            analyze_windows(source, target, spec_x, spec_y, config, window_starts[:wi])
+            analyze_pair(source, target, spec_x, spec_y, _at_window(config, win))
+            raise  # pragma: no cover (analyze_pair raised above)
+    reps, s = target.n_repetitions, config.n_surrogates
+    if not windows:
+        return []
+    if config.strict_permutation and reps < 2:
+        # originals of the first window, then InvalidPermutation (inference.py:147,161)
+        analyze_pair(source, target, spec_x, spec_y, _at_window(config, windows[0]))
     grid = config.test_grid or config.u_candidates
     us = list(config.u_candidates)
-    windows = [(int(t), int(t) + w - 1) for t in window_starts]
-    for lo, hi in windows:
-        for u in us:
-            check_assembly(source, target, spec_x, spec_y, u, (lo, hi))
     pipe = PairPipeline(source, target, spec_x, spec_y, config)
-    reps, s = target.n_repetitions, config.n_surrogates
-    perms = [cached_permutation(config.seed, i, reps, config.strict_permutation) for i in range(s)]
-    pipe.set_perms(perms)
+    pipe.set_perms(surrogate_perms(config.seed, s, reps, config.strict_permutation))
     per_win = np.array([(u, -1) for u in us] + [(u, i) for u in grid for i in range(s)],
                        dtype=np.int32).reshape(-1, 2)
     starts = np.array([lo for lo, _ in windows], dtype=np.int32)
@@ -370,27 +363,30 @@ def analyze_windows(source: EnsembleSeries, target: EnsembleSeries, spec_x: Embe
                              te_all[:, :len(us)], te_all[:, len(us):].reshape(len(windows), len(grid), s))
 
 
+def _at_window(config, win):
+    import dataclasses
+    return dataclasses.replace(config, window=tuple(win))
+
+
 def _assemble_results(source, target, config, windows, us, grid, te_orig, te_surr) -> list:
-    """_assemble_result for many windows at once (same values: the per-window
-    statistics of inference.py:153-193 as array operations over windows)."""
+    """The host statistics of analyze_pair (inference.py:153-193) for many
+    windows: te_orig [windows, len(us)], te_surr [windows, len(grid), S]."""
     s = config.n_surrogates
     te_orig = np.asarray(te_orig, dtype=np.float64)
     # surrogate statistic: running np.maximum over the grid rows from -inf
     surrogates = np.full((len(windows), s), -np.inf)
     for g in range(len(grid)):
         np.maximum(surrogates, te_surr[:, g, :], out=surrogates)
-    in_grid = [i for i, u in enumerate(us) if u in grid]
     medians = np.median(surrogates, axis=1)
     results = []
-    for wi, (lo, hi) in enumerate(windows):
+    for wi, win in enumerate(windows):
         curve = [(u, float(t)) for u, t in zip(us, te_orig[wi])]
         u_best, te_best = max(curve, key=lambda ut: (ut[1], -ut[0]))
-        stat_orig = max(curve[i][1] for i in in_grid)
-        hits = int(np.count_nonzero(surrogates[wi] >= stat_orig))
-        p = (hits + 1) / (s + 1) if config.conservative_pvalue else hits / s
+        stat_orig = max(t for u, t in curve if u in grid)
+        p = permutation_pvalue(stat_orig, surrogates[wi], config.conservative_pvalue)
         sig = p < config.alpha
         results.append(TEResult(source=source.channel_name, target=target.channel_name,
-                                window=(lo, hi), u_selected=u_best, te_value=te_best,
+                                window=win, u_selected=u_best, te_value=te_best,
                                 surrogate_values=surrogates[wi].copy(), p_value=p, significant=sig,
                                 significant_corrected=sig,
                                 te_minus_median_surrogate=te_best - float(medians[wi]),
@@ -404,21 +400,9 @@ def _width(config) -> int:
 
 def _assemble_result(source, target, config, us, grid, te_orig, te_surr) -> TEResult:
     """Host statistics of analyze_pair (inference.py:153-193) for one window."""
-    s = config.n_surrogates
-    curve = [(u, float(t)) for u, t in zip(us, te_orig)]
-    u_best, te_best = max(curve, key=lambda ut: (ut[1], -ut[0]))
-    stat_orig = max(t for u, t in curve if u in grid)
-    surrogates = np.full(s, -np.inf)
-    for row in te_surr:
-        np.maximum(surrogates, row, out=surrogates)
-    p = permutation_pvalue(stat_orig, surrogates, config.conservative_pvalue)
-    sig = p < config.alpha
-    return TEResult(source=source.channel_name, target=target.channel_name,
-                    window=config.window, u_selected=u_best, te_value=te_best,
-                    surrogate_values=surrogates, p_value=p, significant=sig,
-                    significant_corrected=sig,
-                    te_minus_median_surrogate=te_best - float(np.median(surrogates)),
-                    te_curve=curve)
+    te_surr = np.asarray(te_surr, dtype=np.float64).reshape(1, len(grid), config.n_surrogates)
+    return _assemble_results(source, target, config, [config.window], us, grid,
+                             np.asarray(te_orig, dtype=np.float64)[None], te_surr)[0]
 
 
 def scan_delays(source, target, spec_x, spec_y, config) -> TEResult:

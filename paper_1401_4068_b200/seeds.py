@@ -145,10 +145,17 @@ def pcg_states(seeds) -> np.ndarray:
 def surrogate_permutations(master_seed, count: int, reps: int, strict: bool) -> np.ndarray:
     """draw_permutation(reps, SeedSequence((master_seed, i)), strict) for i < count,
     as an int32 [count, reps] array (inference.py:41-49, 101-102, 161-164)."""
+    return surrogate_permutations_at(master_seed, np.arange(count), reps, strict)
+
+
+def surrogate_permutations_at(master_seed, indices, reps: int, strict: bool) -> np.ndarray:
+    """The same for the surrogate indices given, [len(indices), reps] int32."""
+    indices = np.asarray(indices, dtype=np.int64).reshape(-1)
+    count = len(indices)
     out = np.empty((count, reps), dtype=np.int32)
     if count == 0:
         return out
-    words, offsets = _tuple_words(master_seed, np.arange(count))
+    words, offsets = _tuple_words(master_seed, indices)
     nat.check(nat.lib().ente_draw_permutations(
         words.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
         offsets.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), count, int(reps), int(bool(strict)),

@@ -15,7 +15,9 @@ Inputs are the reference's own objects (Chunk, PointSetBundle, numpy seeds);
 the replacements read only their public attributes (`points`, `joint`,
 `n_rows`, `dims`), so they take reference objects as they are.  Results come
 back as this package's NeighborCounts (same fields, same dtypes) and plain
-floats, which the reference code consumes unchanged.
+floats, which the reference code consumes unchanged; errors (raised, or
+returned per slot by batch_search) are re-issued as the reference's own
+exception classes (ente.exceptions) with the same messages.
 """
 
 from __future__ import annotations
@@ -25,15 +27,48 @@ import importlib
 from . import engine as _engine
 from . import ksg as _ksg
 
+def _translate(exc):
+    """The reference's exception of the same name (ente.exceptions), same message:
+    callers of the reference test `isinstance(e, ente.exceptions.KTooLarge)`."""
+    from . import exceptions as ours
+    if isinstance(exc, ours.EnteError):
+        ref = importlib.import_module("ente.exceptions")
+        cls = getattr(ref, type(exc).__name__, None)
+        if cls is not None:
+            out = cls(*exc.args)
+            out.__cause__ = exc
+            return out
+    return exc
+
+
+def _wrap(fn, slots=False):
+    """Call fn; translate raised errors (and, for batch_search, per-slot ones)."""
+    import functools
+
+    @functools.wraps(fn)
+    def call(*args, **kwargs):
+        try:
+            out = fn(*args, **kwargs)
+        except Exception as exc:  # noqa: BLE001 - re-raised as the reference's type
+            tr = _translate(exc)
+            if tr is exc:
+                raise
+            raise tr from exc
+        if slots:
+            out = [_translate(r) if isinstance(r, Exception) else r for r in out]
+        return out
+    return call
+
+
 _PATCHES = {
-    "ente.engine": {"batch_search": _engine.batch_search,
-                    "knn_kth_distances": _engine.knn_kth_distances,
-                    "radius_counts": _engine.radius_counts},
-    "ente.ksg": {"batch_search": _engine.batch_search,
-                 "estimate_te_batch": _ksg.estimate_te_batch,
-                 "estimate_te": _ksg.estimate_te},
-    "ente.bench": {"batch_search": _engine.batch_search},
-    "ente.inference": {"estimate_te_batch": _ksg.estimate_te_batch},
+    "ente.engine": {"batch_search": _wrap(_engine.batch_search, slots=True),
+                    "knn_kth_distances": _wrap(_engine.knn_kth_distances),
+                    "radius_counts": _wrap(_engine.radius_counts)},
+    "ente.ksg": {"batch_search": _wrap(_engine.batch_search, slots=True),
+                 "estimate_te_batch": _wrap(_ksg.estimate_te_batch),
+                 "estimate_te": _wrap(_ksg.estimate_te)},
+    "ente.bench": {"batch_search": _wrap(_engine.batch_search, slots=True)},
+    "ente.inference": {"estimate_te_batch": _wrap(_ksg.estimate_te_batch)},
 }
 
 

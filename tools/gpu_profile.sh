@@ -17,5 +17,6 @@ timeout 1500 ncu --set full --clock-control none --import-source on -k regex:'kn
     > gpurun_out/${tag}_ncu.log 2>&1
 echo "ncu rc=$?"; tail -3 gpurun_out/${tag}_ncu.log
 python tools/ncu_summary.py gpurun_out/${tag}_prof.ncu-rep > gpurun_out/${tag}_ncu_summary.txt 2>&1
-python tools/ncu_summary.py gpurun_out/${tag}_prof.ncu-rep --traffic > gpurun_out/${tag}_ncu_traffic.json 2>&1
+python tools/ncu_summary.py gpurun_out/${tag}_prof.ncu-rep --traffic --merge profiles/ncu_traffic.json --config $cfg > gpurun_out/${tag}_ncu_traffic.json 2>&1
+cp profiles/ncu_traffic.json gpurun_out/${tag}_ncu_traffic_all.json
 cat gpurun_out/${tag}_ncu_traffic.json

@@ -25,6 +25,16 @@ if "--traffic" in sys.argv:  # {kernel: dram read+write bytes per launch} for be
         for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             tot += float(d[k].replace(",", "")) * scale.get(units[hdr.index(k)], 1)
         res.setdefault(name, tot)
+    if "--merge" in sys.argv:  # --merge <traffic.json> --config <C>: res under that config key
+        path = sys.argv[sys.argv.index("--merge") + 1]
+        cfg = sys.argv[sys.argv.index("--config") + 1]
+        try:
+            cur = json.load(open(path))
+        except OSError:
+            cur = {}
+        cur.setdefault(cfg, {}).update(res)
+        cur[cfg]["_capture"] = sys.argv[1]
+        json.dump(cur, open(path, "w"), indent=1)
     print(json.dumps(res))
     sys.exit(0)
 for r in rows[2:]:
