@@ -142,19 +142,30 @@ int ente_ragwitz_errors(const double *values, int reps, int n_samp, int d, int t
 
 /* ---------------------------------------------------------------------------
  * ente_radius_counts -- strict counts #{j != i : maxnorm_marg(p_i, p_j) < r_i}
- * for caller-given radii (fp64, exact), one count array per marginal.
+ * for caller-given radii (fp64, exact), one count array per marginal.  Every
+ * marginal of <= 17 columns runs the fp32-filter count sweep (the marginal
+ * copied into a compiled layout, fp64 settlement of the band); wider ones
+ * the fp64 scan.  ente_search uses the same path for marginal lists that are
+ * not the TE layout (arbitrary column subsets, engine.py:191-200).
  *
  * Replaces: ente.engine.radius_counts         engine.py:179-188
  *
  *   radii        [dev]  [total_rows] fp64, >= 0 (the host raises ShapeMismatch
  *                       for negative radii, engine.py:185-186)
  *   out_counts   [dev]  [n_marg x total_rows] int32
+ *   workspace           ente_radius_counts_workspace_size(chunks, n_chunks, dim)
  * ------------------------------------------------------------------------- */
-size_t ente_radius_counts_workspace_size(int n_chunks);
+size_t ente_radius_counts_workspace_size(const ente_chunk *chunks, int n_chunks, int dim);
 int ente_radius_counts(const double *pts64, int64_t total_rows, int dim, const ente_chunk *chunks,
                        int n_chunks, const uint32_t *marg_masks, int n_marg, const double *radii,
                        int32_t *out_counts, int32_t *status, void *workspace, size_t ws_bytes,
                        void *stream);
+
+/* ente_search_path -- which engine ente_search runs for this layout:
+ * 1 the TE-layout fp32 sweeps, 2 the kNN sweep + generic marginal count
+ * sweeps, 0 the fp64 warp-per-point scan (O(n^2), no pruning) -- so hosts can
+ * report the slow case instead of taking it silently. */
+int ente_search_path(int dim, const uint32_t *marg_masks, int n_marg, int k);
 
 /* ---------------------------------------------------------------------------
  * ente_jitter -- tie-breaking jitter, in place:
@@ -250,6 +261,12 @@ int ente_seed_states(const uint32_t *words, const int64_t *offsets, int64_t n_it
                      uint64_t *out);
 int ente_draw_permutations(const uint32_t *words, const int64_t *offsets, int64_t n_perms,
                            int reps, int strict, int32_t *out);
+
+/* ente_host_gather -- multi-threaded concatenation of n host buffers
+ * (srcs[i], bytes[i]) into dst (pinned staging for one H2D copy of a batch).
+ * Replaces the per-chunk host copies of batch_search's inputs
+ * (engine.py:203-216 loops over chunks one at a time). */
+int ente_host_gather(const void *const *srcs, const int64_t *bytes, int64_t n, void *dst);
 
 /* ---------------------------------------------------------------------------
  * Instrumentation (no reference counterpart: the reference only has

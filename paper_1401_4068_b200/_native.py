@@ -49,7 +49,8 @@ def _declare(L):
         "ente_knn_indices": ([vp, i64, i32, cp, i32, i32, vp, vp, vp, vp, sz, vp], i32),
         "ente_search_split": ([vp, i64, i32, cp, i32, u32p, i32, i32, i32, i32, vp, vp, vp, vp, sz,
                                vp], i32),
-        "ente_radius_counts_workspace_size": ([i32], sz),
+        "ente_radius_counts_workspace_size": ([cp, i32, i32], sz),
+        "ente_search_path": ([i32, u32p, i32, i32], i32),
         "ente_radius_counts": ([vp, i64, i32, cp, i32, u32p, i32, vp, vp, vp, vp, sz, vp], i32),
         "ente_jitter_workspace_size": ([i32, i32], sz),
         "ente_jitter": ([vp, i32, cp, i32, u64p, dbl, vp, vp, sz, vp], i32),
@@ -66,6 +67,7 @@ def _declare(L):
         "ente_microbench_pce": ([i32, i32, ctypes.POINTER(dbl), vp], i32),
         "ente_search_work": ([ctypes.POINTER(ctypes.c_ulonglong)] * 2, None),
         "ente_seed_states": ([u32p, ctypes.POINTER(i64), i64, u64p], i32),
+        "ente_host_gather": ([ctypes.POINTER(vp), ctypes.POINTER(i64), i64, vp], i32),
         "ente_draw_permutations": ([u32p, ctypes.POINTER(i64), i64, i32, i32, i32p], i32),
     }
     for name, (args, res) in sig.items():

@@ -1133,16 +1133,18 @@ static int validate(const ente_chunk *chunks, int n_chunks, int dim, const uint3
 // prep -> principal axes -> both sort orders -> both fp32 copies with boxes
 static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Plan &p,
                          const SearchWs &w, int n_chunks, int32_t *status, int prune,
-                         int allow_pca = 1) {
+                         int allow_pca = 1, bool count_only = false) {
         ENTE_LAUNCH("prep", st,
                     (p.max_npad <= kPrepSmallN ? prep_kernel<kPrepThreadsSmall> : prep_kernel<kPrepThreadsBig>)
                     <<<n_chunks, p.max_npad <= kPrepSmallN ? kPrepThreadsSmall : kPrepThreadsBig, 0, st>>>(
                         pts64, dim, w.info, w.stats, status, 1));
         ENTE_CUDA(cudaGetLastError());
-        ENTE_LAUNCH("axes", st,
-                    axes_kernel<<<(n_chunks + 127) / 128, 128, 0, st>>>(w.info, n_chunks, dim, w.stats,
-                                                                        allow_pca));
-        ENTE_CUDA(cudaGetLastError());
+        if (!count_only) {
+            ENTE_LAUNCH("axes", st,
+                        axes_kernel<<<(n_chunks + 127) / 128, 128, 0, st>>>(w.info, n_chunks, dim,
+                                                                            w.stats, allow_pca));
+            ENTE_CUDA(cudaGetLastError());
+        }
         FilterCols sfc = p.fc;
         if (!prune) sfc.nf = 0;  // identity order
         ENTE_LAUNCH("sort", st,
@@ -1150,6 +1152,15 @@ static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Pl
                     <<<n_chunks, p.max_npad <= kSortSmallN ? kSortThreadsSmall : kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats, sfc,
                                                                    w.ka, w.kb, w.va, w.vb, w.perm));
         ENTE_CUDA(cudaGetLastError());
+        if (count_only) {  // the count order alone: no kNN-order copy
+            dim3 ggrid((unsigned)(p.max_npad / kTJ), (unsigned)std::min(n_chunks, 65535));
+            ENTE_LAUNCH("gather", st,
+                        gather_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.stats,
+                                                             w.perm, p.dp, p.fc, w.pts32, w.fbox,
+                                                             w.inv));
+            ENTE_CUDA(cudaGetLastError());
+            return ENTE_OK;
+        }
         ENTE_LAUNCH("sort_pca", st,
                     (p.max_npad <= kSortSmallN ? sort_pca_kernel<kSortThreadsSmall> : sort_pca_kernel<kSortThreads>)
                     <<<n_chunks, p.max_npad <= kSortSmallN ? kSortThreadsSmall : kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats,
@@ -1214,6 +1225,8 @@ static int upload_chunks(cudaStream_t st, const ente_chunk *chunks, int n_chunks
 
 using namespace ente;
 
+static size_t radius_ws_size(const ente_chunk *chunks, int n_chunks, int max_mc);
+
 extern "C" size_t ente_search_workspace_size(const ente_chunk *chunks, int n_chunks, int dim,
                                              int n_marg, int k) {
     (void)n_marg;
@@ -1226,7 +1239,9 @@ extern "C" size_t ente_search_workspace_size(const ente_chunk *chunks, int n_chu
     }
     Arena a(nullptr, 0);
     layout_ws(a, p, n_chunks);
-    return a.used + 256;
+    // marginals outside the TE layout run the generic radius path
+    const size_t gen = n_marg > 0 ? radius_ws_size(chunks, n_chunks, std::min(dim, 17)) : 0;
+    return std::max(a.used, gen) + 256;
 }
 
 static int g_prune = -1;  // ENTE_PRUNE=0 disables box pruning (measurement only)
@@ -1256,6 +1271,207 @@ static unsigned long long *device_work() {
     return g_dwork[dev];
 }
 
+// ---------------------------------------------------------------------------
+// Generic marginal counts with given radii (reference radius_counts,
+// engine.py:179-188, and _search_one's arbitrary marginal column lists,
+// engine.py:191-200): the marginal's columns are copied into a dense fp64
+// matrix laid out as a compiled TE layout [0 | gate (DY) | rest (DX)] whose
+// slot-2 marginal (columns 1 .. D'-1) is exactly the marginal (zero columns
+// pad it to a compiled width; they add nothing to a max-norm).  The count
+// order, fp32 copy, boxes and count_pass sweep of the TE path then run
+// unchanged with the band centred on fl32(r_i): |fl32(r) - r| <= u32 r, and
+// for r <= 4 s that is <= delta, so v32 < lo => v64 < r and v32 > hi =>
+// v64 > r still hold (for r > 4 s every pair is inside, which lo already
+// says); band events are settled in fp64 by resolve_counts, overflowing
+// references by the exact kernel.
+// ---------------------------------------------------------------------------
+struct MargCols {
+    int n;
+    int col[kMaxDim];
+};
+
+// dense [total_rows x dd] fp64: column 0 and columns > n hold 0
+__global__ void __launch_bounds__(256) marg_dense_kernel(const double *__restrict__ pts64, int dim,
+                                                         int64_t total_rows, MargCols mc, int dd,
+                                                         double *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total_rows * dd;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / dd;
+        const int c = (int)(i - row * dd);
+        out[i] = (c >= 1 && c <= mc.n) ? pts64[row * dim + mc.col[c - 1]] : 0.0;
+    }
+}
+
+// band centres in the count order: t32[sorted position] = fl32(radius of its row)
+__global__ void __launch_bounds__(kWarpRefs) radii_t32_kernel(
+    const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks,
+    const int32_t *__restrict__ perm, const double *__restrict__ radii, float *__restrict__ t32) {
+    const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
+    const ChunkInfo ci = info[tr.chunk];
+    const int s = tr.r0 + threadIdx.x;
+    if (s >= ci.n || !ci.ok32) return;
+    const int64_t srow = ci.row0 + s;
+    t32[srow] = __double2float_rn(radii[ci.row0 + perm[srow]]);
+}
+
+// certain count + fp64 settlement of the band events of the slot-2 marginal
+__global__ void __launch_bounds__(kWarpRefs) resolve_counts_kernel(
+    const double *__restrict__ dense, int dd, const ChunkInfo *__restrict__ info,
+    const int32_t *__restrict__ tile0, int n_chunks, const int32_t *__restrict__ perm,
+    const double *__restrict__ radii, const int32_t *__restrict__ cnt_in,
+    const uint32_t *__restrict__ ev, const int32_t *__restrict__ ev_n, int64_t ws_rows,
+    int32_t *__restrict__ out, int64_t *__restrict__ ovf_list, int32_t *__restrict__ ovf_n) {
+    const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
+    const ChunkInfo ci = info[tr.chunk];
+    const int s = tr.r0 + threadIdx.x;
+    if (s >= ci.n) return;
+    const int64_t srow = ci.row0 + s;
+    const int64_t row = ci.ok32 ? ci.row0 + perm[srow] : srow;
+    const int ne = ci.ok32 ? ev_n[srow] : kCap + 1;
+    if (ne > kCap) {
+        ovf_list[atomicAdd(ovf_n, 1)] = row;
+        return;
+    }
+    const double r = radii[row];
+    const double *rp = dense + row * dd;
+    int cnt = cnt_in[2 * ws_rows + srow];
+    for (int e = 0; e < ne; ++e) {
+        const uint32_t w = ev[srow * kCap + e];
+        const int j = (int)(w & 0x0FFFFFFFu);
+        if (j == s || !((w >> 28) & 4u)) continue;
+        const double *q = dense + (ci.row0 + perm[ci.row0 + j]) * dd;
+        double d = 0.0;
+        for (int c = 1; c < dd; ++c) d = fmax(d, fabs(__dsub_rn(rp[c], q[c])));
+        cnt += d < r;
+    }
+    out[row] = cnt;
+}
+
+// compiled TE layout (DY, DX) whose columns 1 .. DY + DX hold an mc-column
+// marginal: 1 <= DY <= min(mc, kGate), DY + DX >= mc, fewest columns, DY
+// nearest 3 (the gate width the count order and boxes work best with)
+static bool marg_layout(int mc, int &dy, int &dx) {
+    static const int pref[4] = {3, 4, 2, 1};
+    for (int t = mc; t + 1 <= 18; ++t)
+        for (int y : pref) {
+            if (y > mc || y > t) continue;
+            if (count_table(y, t - y, 0) != nullptr) {
+                dy = y;
+                dx = t - y;
+                return true;
+            }
+        }
+    return false;
+}
+
+static Plan radius_plan(const ente_chunk *chunks, int n_chunks, int dy, int dx) {
+    Plan p;
+    for (int c = 0; c < n_chunks; ++c) {
+        p.total_rows = std::max(p.total_rows, chunks[c].row0 + chunks[c].n);
+        const int npad = round_up(chunks[c].n, kTJ);
+        p.total_prows += npad;
+        p.max_npad = std::max(p.max_npad, npad);
+        p.n_tiles += (chunks[c].n + kWarpRefs - 1) / kWarpRefs;
+    }
+    p.fast = true;
+    p.dy = dy;
+    p.dx = dx;
+    p.slots = 2;
+    p.dp = (1 + dy + dx + 3) & ~3;
+    p.lay.dy = dy;
+    p.lay.nout = 1;
+    p.lay.slot[0] = 2;
+    p.fc = filter_cols(dy);
+    return p;
+}
+
+// workspace of the generic radius path for marginals of up to max_mc columns
+static size_t radius_ws_size(const ente_chunk *chunks, int n_chunks, int max_mc) {
+    size_t need = 0;
+    for (int mc = 1; mc <= max_mc; ++mc) {
+        int dy, dx;
+        if (!marg_layout(mc, dy, dx)) continue;
+        Plan p = radius_plan(chunks, n_chunks, dy, dx);
+        Arena a(nullptr, 0);
+        layout_ws(a, p, n_chunks);
+        a.take<double>((size_t)p.total_rows * (1 + dy + dx));
+        need = std::max(need, a.used);
+    }
+    return need;
+}
+
+// counts of one marginal (mask) for the given radii; false when no compiled
+// layout holds it (the caller then scans in fp64)
+static int radius_fast(const double *pts64, int64_t total_rows, int dim, const ente_chunk *chunks,
+                       int n_chunks, uint32_t mask, const double *radii, int32_t *out_counts,
+                       int32_t *status, void *workspace, size_t ws_bytes, cudaStream_t st,
+                       bool &done) {
+    done = false;
+    MargCols mc{};
+    for (int c = 0; c < dim; ++c)
+        if ((mask >> c) & 1u) mc.col[mc.n++] = c;
+    int dy = 0, dx = 0;
+    if (mc.n < 1 || !marg_layout(mc.n, dy, dx)) return ENTE_OK;
+    const int dd = 1 + dy + dx;
+    Plan p = radius_plan(chunks, n_chunks, dy, dx);
+    Arena a(workspace, ws_bytes);
+    SearchWs w = layout_ws(a, p, n_chunks);
+    double *dense = a.take<double>((size_t)p.total_rows * dd);
+    if (!a.ok() || !w.info || !dense) {
+        set_error("ente_radius_counts: workspace of %zu bytes too small (need %zu)", ws_bytes, a.used);
+        return ENTE_ERR_WORKSPACE;
+    }
+    std::vector<int32_t> htile0;
+    int32_t ntiles = 0;
+    int rc = upload_chunks(st, chunks, n_chunks, 1, p, w, status, htile0, ntiles);
+    if (rc != ENTE_OK) return rc;
+    ENTE_CUDA(cudaMemcpyAsync(w.tile0, htile0.data(), sizeof(int32_t) * (2 * n_chunks + 1),
+                              cudaMemcpyHostToDevice, st));
+    {
+        const int64_t elems = p.total_rows * dd;
+        const unsigned blocks = (unsigned)std::min<int64_t>((elems + 255) / 256, (int64_t)num_sms() * 32);
+        ENTE_LAUNCH("marg_dense", st,
+                    marg_dense_kernel<<<std::max(1u, blocks), 256, 0, st>>>(pts64, dim, p.total_rows,
+                                                                            mc, dd, dense));
+        ENTE_CUDA(cudaGetLastError());
+    }
+    const int prune = prune_enabled();
+    rc = launch_orders(st, dense, dd, p, w, n_chunks, status, prune, 0, true);
+    if (rc != ENTE_OK) return rc;
+    if (ntiles > 0) {
+        unsigned long long *work = device_work();
+        if (!work) {
+            set_error("ente_radius_counts: cannot allocate the work counters");
+            return ENTE_ERR_CUDA;
+        }
+        const unsigned nt = (unsigned)ntiles;
+        ENTE_LAUNCH("radii_t32", st,
+                    radii_t32_kernel<<<nt, kWarpRefs, 0, st>>>(w.info, w.tile0, n_chunks, w.perm, radii,
+                                                               w.t32));
+        ENTE_CUDA(cudaGetLastError());
+        const CountFn count_fn = count_table(dy, dx, p.max_npad);
+        prefer_shared(reinterpret_cast<const void *>(count_fn));
+        ENTE_LAUNCH("count_pass", st,
+                    count_fn<<<nt, 32, 0, st>>>(w.pts32, w.fbox, w.info, w.tile0, n_chunks, w.t32,
+                                                p.total_rows, prune, w.cnt3, w.ev, w.ev_n, 4u,
+                                                work + 1));
+        ENTE_CUDA(cudaGetLastError());
+        ENTE_LAUNCH("resolve_counts", st,
+                    resolve_counts_kernel<<<nt, kWarpRefs, 0, st>>>(
+                        dense, dd, w.info, w.tile0, n_chunks, w.perm, radii, w.cnt3, w.ev, w.ev_n,
+                        p.total_rows, out_counts, w.ovf, w.ovf_n));
+        ENTE_CUDA(cudaGetLastError());
+        Masks masks{};
+        masks.n = 1;
+        masks.m[0] = mask;
+        launch_exact<4>(st, pts64, dim, w.info, n_chunks, status, w.ovf, w.ovf_n, 0, 1, masks,
+                        total_rows, nullptr, out_counts, radii);
+        ENTE_CUDA(cudaGetLastError());
+    }
+    done = true;
+    return ENTE_OK;
+}
+
 static int search_impl(const double *pts64, int64_t total_rows, int dim, const ente_chunk *chunks,
                        int n_chunks, const uint32_t *marg_masks, int n_marg, int k, double *out_eps,
                        int32_t *out_counts, int32_t *status, void *workspace, size_t ws_bytes,
@@ -1269,6 +1485,31 @@ static int search_impl(const double *pts64, int64_t total_rows, int dim, const e
         set_error("ente_search: chunks reference row %lld beyond total_rows=%lld",
                   (long long)p.total_rows, (long long)total_rows);
         return ENTE_ERR_ARG;
+    }
+    if (!p.fast && n_marg > 0) {
+        // marginals that are not the TE layout's: exact eps from the kNN fast path
+        // (no marginals), then each marginal's counts with those radii
+        uint32_t none[kMaxMarg] = {0};
+        Plan pk = make_plan(chunks, n_chunks, dim, none, 0, k);
+        bool fits = pk.fast;
+        for (int m = 0; m < n_marg && fits; ++m) {
+            int dy, dx;
+            fits = marg_layout(__builtin_popcount(marg_masks[m]), dy, dx);
+        }
+        if (fits) {
+            if (split_count > 1 && split_index != 0) return ENTE_OK;  // part 0 does it all
+            rc = search_impl(pts64, total_rows, dim, chunks, n_chunks, marg_masks, 0, k, out_eps,
+                             nullptr, status, workspace, ws_bytes, stream, 0, 1);
+            if (rc != ENTE_OK) return rc;
+            for (int m = 0; m < n_marg; ++m) {
+                bool done = false;
+                rc = radius_fast(pts64, total_rows, dim, chunks, n_chunks, marg_masks[m], out_eps,
+                                 out_counts + (int64_t)m * total_rows, status, workspace, ws_bytes,
+                                 st, done);
+                if (rc != ENTE_OK) return rc;
+            }
+            return ENTE_OK;
+        }
     }
     const int64_t ws_rows = p.total_rows;  // stride of the workspace per-row arrays
     Arena a(workspace, ws_bytes);
@@ -1447,14 +1688,33 @@ extern "C" int ente_knn_indices(const double *pts64, int64_t total_rows, int dim
     return ENTE_ERR_ARG;
 }
 
-extern "C" size_t ente_radius_counts_workspace_size(int n_chunks) {
+extern "C" int ente_search_path(int dim, const uint32_t *marg_masks, int n_marg, int k) {
+    if (dim < 1 || dim > kMaxDim || n_marg < 0 || n_marg > kMaxMarg || k < 1) return 0;
+    ente_chunk one{0, 1 << 16, 0};
+    Plan p = make_plan(&one, 1, dim, marg_masks, n_marg, k);
+    if (p.fast) return 1;
+    uint32_t none[kMaxMarg] = {0};
+    if (!make_plan(&one, 1, dim, none, 0, k).fast) return 0;
+    for (int m = 0; m < n_marg; ++m) {
+        int dy, dx;
+        if (!marg_layout(__builtin_popcount(marg_masks[m]), dy, dx)) return 0;
+    }
+    return 2;
+}
+
+extern "C" size_t ente_radius_counts_workspace_size(const ente_chunk *chunks, int n_chunks,
+                                                    int dim) {
     Arena a(nullptr, 0);
     a.take<ChunkInfo>(n_chunks);
-    return a.used + 256;
+    a.take<int32_t>(2);
+    const size_t gen = (chunks && dim >= 1) ? radius_ws_size(chunks, n_chunks, std::min(dim, 17)) : 0;
+    return std::max(a.used, gen) + 256;
 }
 
 // Strict radius counts for caller-given radii (reference radius_counts,
-// engine.py:179-188): fp64 warp-per-point scan, one count array per marginal.
+// engine.py:179-188), one count array per marginal: the generic fp32-filter
+// sweep (radius_fast) for every marginal a compiled layout holds, the fp64
+// warp-per-point scan for the others.
 extern "C" int ente_radius_counts(const double *pts64, int64_t total_rows, int dim,
                                   const ente_chunk *chunks, int n_chunks, const uint32_t *marg_masks,
                                   int n_marg, const double *radii, int32_t *out_counts,
@@ -1466,7 +1726,26 @@ extern "C" int ente_radius_counts(const double *pts64, int64_t total_rows, int d
         set_error("ente_radius_counts: radii and out_counts are required");
         return ENTE_ERR_ARG;
     }
+    for (int c = 0; c < n_chunks; ++c)
+        if (chunks[c].row0 + chunks[c].n > total_rows) {
+            set_error("ente_radius_counts: chunk %d beyond total_rows", c);
+            return ENTE_ERR_ARG;
+        }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Masks slow{};
+    std::vector<int> slow_out;
+    for (int m = 0; m < n_marg; ++m) {
+        bool done = false;
+        rc = radius_fast(pts64, total_rows, dim, chunks, n_chunks, marg_masks[m], radii,
+                         out_counts + (int64_t)m * total_rows, status, workspace, ws_bytes, st, done);
+        if (rc != ENTE_OK) return rc;
+        if (!done) {
+            slow.m[slow.n++] = marg_masks[m];
+            slow_out.push_back(m);
+        }
+    }
+    if (slow.n == 0) return ENTE_OK;
+    // marginals no compiled layout holds (more than 17 columns): fp64 scan
     Arena a(workspace, ws_bytes);
     ChunkInfo *info = a.take<ChunkInfo>(n_chunks);
     if (!a.ok() || !info) {
@@ -1479,18 +1758,16 @@ extern "C" int ente_radius_counts(const double *pts64, int64_t total_rows, int d
         hinfo[c] = ChunkInfo{};
         hinfo[c].row0 = chunks[c].row0;
         hinfo[c].n = chunks[c].n;
-        if (chunks[c].row0 + chunks[c].n > total_rows) {
-            set_error("ente_radius_counts: chunk %d beyond total_rows", c);
-            return ENTE_ERR_ARG;
-        }
     }
     ENTE_CUDA(cudaMemcpyAsync(info, hinfo.data(), sizeof(ChunkInfo) * n_chunks, cudaMemcpyHostToDevice, st));
     ENTE_CUDA(cudaMemcpyAsync(status, hstatus.data(), sizeof(int32_t) * n_chunks, cudaMemcpyHostToDevice, st));
-    Masks masks{};
-    masks.n = n_marg;
-    for (int m = 0; m < n_marg; ++m) masks.m[m] = marg_masks[m];
-    launch_exact<4>(st, pts64, dim, info, n_chunks, status, nullptr, nullptr, total_rows, 1, masks,
-                    total_rows, nullptr, out_counts, radii);
-    ENTE_CUDA(cudaGetLastError());
+    for (int i = 0; i < slow.n; ++i) {
+        Masks one{};
+        one.n = 1;
+        one.m[0] = slow.m[i];
+        launch_exact<4>(st, pts64, dim, info, n_chunks, status, nullptr, nullptr, total_rows, 1, one,
+                        total_rows, nullptr, out_counts + (int64_t)slow_out[i] * total_rows, radii);
+        ENTE_CUDA(cudaGetLastError());
+    }
     return ENTE_OK;
 }

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "ente_b200.h"
+#include "hostutil.cuh"
 
 namespace ente {
 void set_error(const char *fmt, ...);
@@ -131,23 +132,6 @@ struct Pcg64 {
     }
 };
 
-template <class F>
-void parallel_for(int64_t n, int64_t grain, F &&f) {
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const int64_t nt = std::min<int64_t>(hw, (n + grain - 1) / grain);
-    if (nt <= 1) {
-        f(0, n);
-        return;
-    }
-    std::vector<std::thread> th;
-    const int64_t per = (n + nt - 1) / nt;
-    for (int64_t t = 0; t < nt; ++t) {
-        const int64_t lo = t * per, hi = std::min(n, lo + per);
-        if (lo < hi) th.emplace_back([&f, lo, hi] { f(lo, hi); });
-    }
-    for (auto &t : th) t.join();
-}
-
 }  // namespace
 
 extern "C" {
@@ -163,7 +147,7 @@ int ente_seed_states(const uint32_t *words, const int64_t *offsets, int64_t n_it
             ente::set_error("ente_seed_states: offsets must be non-decreasing");
             return ENTE_ERR_ARG;
         }
-    parallel_for(n_items, 4096, [&](int64_t lo, int64_t hi) {
+    ente::parallel_for(n_items, 4096, [&](int64_t lo, int64_t hi) {
         for (int64_t i = lo; i < hi; ++i) {
             uint64_t s[4];
             seed_sequence_state(words + offsets[i], offsets[i + 1] - offsets[i], s);
@@ -188,7 +172,7 @@ int ente_draw_permutations(const uint32_t *words, const int64_t *offsets, int64_
         ente::set_error("strict permutation needs R >= 2");
         return ENTE_ERR_ARG;
     }
-    parallel_for(n_perms, 16, [&](int64_t lo, int64_t hi) {
+    ente::parallel_for(n_perms, 16, [&](int64_t lo, int64_t hi) {
         std::vector<int64_t> a((size_t)reps);
         for (int64_t p = lo; p < hi; ++p) {
             uint64_t s[4];

@@ -279,7 +279,8 @@ struct Walker {
                 base += 32;
                 wst = nst;
                 wd = wst >= 0 ? dist(nb) : INFINITY;
-                mask = __ballot_sync(0xffffffffu, strict ? (wd < bound) : (wd <= bound));
+                // (positions past the chunk never qualify, even for an infinite bound)
+                mask = __ballot_sync(0xffffffffu, wst >= 0 && (strict ? (wd < bound) : (wd <= bound)));
                 prefetch(fb, base + 32 + lane);
             }
             const int b = __ffs(mask) - 1;

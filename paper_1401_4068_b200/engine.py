@@ -14,8 +14,10 @@ bit-identical to the reference's fp64 sweep.
 
 from __future__ import annotations
 
+import ctypes
 import os
 import threading
+import warnings
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -78,11 +80,34 @@ def column_mask(cols, dim: int) -> int:
     return mask
 
 
+class SlowPathWarning(RuntimeWarning):
+    """A search layout runs the fp64 O(n^2) scan instead of the pruned fp32 sweeps."""
+
+
+_PATHS: dict = {}
+
+
+def search_path(dim: int, masks, k: int) -> int:
+    """ente_search_path: 1 TE-layout sweeps, 2 kNN sweep + generic marginal
+    counts, 0 the fp64 scan (warned once per layout: it is O(n^2) unpruned)."""
+    key = (dim, tuple(masks), k)
+    path = _PATHS.get(key)
+    if path is None:
+        path = int(nat.lib().ente_search_path(int(dim), nat.masks_array(masks), len(masks),
+                                              int(k)))
+        _PATHS[key] = path
+        if path == 0:
+            warnings.warn(f"dim={dim}, marginal masks {[hex(m) for m in masks]}, k={k}: no compiled "
+                          "sweep layout; this search runs the fp64 O(n^2) scan", SlowPathWarning,
+                          stacklevel=3)
+    return path
+
+
 # ---------------------------------------------------------------------------
 # device-level entry points (tensors in, tensors out; used by ksg / bench)
 # ---------------------------------------------------------------------------
 def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int, reuse: bool = False,
-                  tag: str = "", split=None):
+                  tag: str = "", split=None, split_fill=(0.0, 0)):
     """ente_search on a device-resident [rows, dim] fp64 matrix.
 
     Returns (eps [rows] f64, counts [n_marg, rows] int32, status [n_chunks] int32),
@@ -109,9 +134,9 @@ def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int, reuse: bool = F
         nat.check(L.ente_search(nat.ptr(pts64), rows, dim, table, len(ns), marr, len(masks),
                                 int(k), nat.ptr(eps), nat.ptr(counts), nat.ptr(status),
                                 nat.ptr(ws), ws.numel(), nat.stream_handle()), "ente_search")
-    else:  # (index, count): this part's references only, other rows zeroed
-        eps.zero_()
-        counts.zero_()
+    else:  # (index, count): this part's references only, other rows = split_fill
+        eps.fill_(split_fill[0])
+        counts.fill_(split_fill[1])
         nat.check(L.ente_search_split(nat.ptr(pts64), rows, dim, table, len(ns), marr, len(masks),
                                       int(k), int(split[0]), int(split[1]), nat.ptr(eps),
                                       nat.ptr(counts), nat.ptr(status), nat.ptr(ws), ws.numel(),
@@ -136,36 +161,53 @@ def _pinned_buffer(nbytes: int) -> torch.Tensor:
 
 
 def _upload(points_list):
-    """Concatenate the chunks straight into pinned memory and copy them to the device."""
+    """Concatenate the chunks straight into pinned memory (multi-threaded,
+    ente_host_gather) and copy them to the device in one transfer."""
     rows = sum(p.shape[0] for p in points_list)
     dim = points_list[0].shape[1]
     stage = _pinned_buffer(rows * dim * 8)[:rows * dim * 8].view(torch.float64).view(rows, dim)
-    np.concatenate(points_list, axis=0, out=stage.numpy())
+    if len(points_list) == 1:
+        np.copyto(stage.numpy(), points_list[0])
+    else:
+        n = len(points_list)
+        srcs = (ctypes.c_void_p * n)(*[p.ctypes.data for p in points_list])
+        sizes = np.fromiter((p.nbytes for p in points_list), dtype=np.int64, count=n)
+        nat.check(nat.lib().ente_host_gather(srcs, sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                             n, stage.data_ptr()), "ente_host_gather")
     dev = nat.scratch("engine.points", (rows, dim), torch.float64)
     dev.copy_(stage, non_blocking=True)
     return dev
 
 
 def _run_group(points_list, dim, masks, k):
+    search_path(dim, masks, k)
     ns = np.fromiter((p.shape[0] for p in points_list), dtype=np.int64, count=len(points_list))
     rows0 = np.concatenate([[0], np.cumsum(ns)[:-1]]).astype(np.int64)
     dev = _upload(points_list)
     eps, counts, status = search_device(dev, rows0, ns, masks, k, reuse=True)
-    eps_h = eps.cpu().numpy()
-    cnt_h = counts.cpu().numpy().astype(np.int64)
-    st_h = status.cpu().numpy()
-    out = []
+    # results land in fresh pinned host tensors (torch's caching host allocator:
+    # no page-locking or first-touch per call), counts widened to int64 on the
+    # device, so the host does no conversion pass
     nm = len(masks)
-    for i in range(len(points_list)):
-        r0, n = int(rows0[i]), int(ns[i])
-        if st_h[i] == nat.CHUNK_NONFINITE:
+    eps_p = torch.empty(eps.shape, dtype=torch.float64, pin_memory=True)
+    eps_p.copy_(eps, non_blocking=True)
+    cnt_p = torch.empty(counts.shape, dtype=torch.int64, pin_memory=True)
+    if nm:
+        cnt_p.copy_(counts.to(torch.int64), non_blocking=True)
+    st_h = status.cpu().numpy()  # synchronises the stream
+    eps_h, cnt_h = eps_p.numpy(), cnt_p.numpy()
+    rows = [cnt_h[m] for m in range(nm)]
+    out = []
+    for i, (r0, n) in enumerate(zip(rows0.tolist(), ns.tolist())):
+        code = st_h[i]
+        if code == nat.CHUNK_NONFINITE:
             out.append(ShapeMismatch("chunk contains non-finite values"))
-        elif st_h[i] == nat.CHUNK_K_TOO_LARGE:
+        elif code == nat.CHUNK_K_TOO_LARGE:
             out.append(KTooLarge(f"k={k} not in [1, n-1] for n={n}"))
         else:
             # views into this call's fresh result arrays (nothing else holds them)
-            out.append(NeighborCounts(eps_h[r0:r0 + n],
-                                      tuple(cnt_h[m, r0:r0 + n] for m in range(nm))))
+            end = r0 + n
+            out.append(NeighborCounts(eps_h[r0:end], tuple([r[r0:end] for r in rows])))
     return out
 
 
@@ -177,6 +219,11 @@ def batch_search(items: Sequence, k: int):
     Chunks sharing (dim, marginal layout) go to the GPU in one launch sequence.
     """
     results = [None] * len(items)
+    fast = _uniform_batch(items, k)
+    if fast is not None:  # one validated layout for every chunk: no per-item checks
+        dim, masks, pts_list = fast
+        _run_waves(list(enumerate(pts_list)), dim, masks, k, results)
+        return results
     groups = {}
     mask_cache = {}  # (id(marginals), dim) -> (marginals, masks): items usually share one list
     for slot, (chunk, marginals) in enumerate(items):
@@ -204,20 +251,47 @@ def batch_search(items: Sequence, k: int):
             continue
         groups.setdefault((dim, masks), []).append((slot, pts))
     for (dim, masks), members in groups.items():
-        # device waves of at most MAX_WAVE_ROWS points (the search workspace is
-        # a few hundred bytes per point)
-        start = 0
-        while start < len(members):
-            stop, rows = start, 0
-            while stop < len(members) and (stop == start or rows + len(members[stop][1]) <= MAX_WAVE_ROWS):
-                rows += len(members[stop][1])
-                stop += 1
-            wave = members[start:stop]
-            outs = _run_group([p for _, p in wave], dim, list(masks), k)
-            for (slot, _), res in zip(wave, outs):
-                results[slot] = res
-            start = stop
+        _run_waves(members, dim, masks, k, results)
     return results
+
+
+def _uniform_batch(items, k):
+    """(dim, masks, points) when every item is a Chunk of one width sharing one
+    marginal list object with k in range -- the batch_search calls of the
+    estimator and the bench -- so the per-item checks can be skipped."""
+    if not items:
+        return None
+    first = items[0][1]
+    if any(m is not first for _, m in items) or not all(type(c) is Chunk for c, _ in items):
+        return None
+    pts_list = [c.points for c, _ in items]  # Chunk validated these (fp64, contiguous, finite)
+    shapes = np.array([p.shape for p in pts_list], dtype=np.int64)
+    dim = int(shapes[0, 1])
+    if (shapes[:, 1] != dim).any() or k < 1 or k > int(shapes[:, 0].min()) - 1:
+        return None
+    try:
+        masks = tuple(column_mask(cols, dim) for cols in first)
+    except ShapeMismatch:
+        return None
+    if dim > MAX_DIM or k > MAX_K or len(masks) > MAX_MARG:
+        return None
+    return dim, masks, pts_list
+
+
+def _run_waves(members, dim, masks, k, results):
+    """Device waves of at most MAX_WAVE_ROWS points (the search workspace is a
+    few hundred bytes per point); members are (slot, points) pairs."""
+    start = 0
+    while start < len(members):
+        stop, rows = start, 0
+        while stop < len(members) and (stop == start or rows + len(members[stop][1]) <= MAX_WAVE_ROWS):
+            rows += len(members[stop][1])
+            stop += 1
+        wave = members[start:stop]
+        outs = _run_group([p for _, p in wave], dim, list(masks), k)
+        for (slot, _), res in zip(wave, outs):
+            results[slot] = res
+        start = stop
 
 
 def knn_kth_distances(chunk: Chunk, k: int) -> np.ndarray:
@@ -279,6 +353,9 @@ def radius_counts(chunk: Chunk, radii) -> np.ndarray:
         raise ShapeMismatch("radii must be nonnegative")
     if dim > MAX_DIM:
         raise NotImplementedError(f"dim={dim} exceeds {MAX_DIM}")
+    if dim > 17:
+        warnings.warn(f"radius_counts over {dim} columns: no compiled sweep layout; this runs the "
+                      "fp64 O(n^2) scan", SlowPathWarning, stacklevel=2)
     L = nat.lib()
     dev = _upload([pts])
     r = torch.from_numpy(radii).to(dev.device)
@@ -286,7 +363,7 @@ def radius_counts(chunk: Chunk, radii) -> np.ndarray:
     status = torch.empty(1, dtype=torch.int32, device=dev.device)
     table = nat.chunk_table([0], [n])
     marr = nat.masks_array([(1 << dim) - 1])
-    ws = nat.workspace(L.ente_radius_counts_workspace_size(1))
+    ws = nat.workspace(L.ente_radius_counts_workspace_size(table, 1, dim))
     nat.check(L.ente_radius_counts(nat.ptr(dev), n, dim, table, 1, marr, 1, nat.ptr(r),
                                    nat.ptr(counts), nat.ptr(status), nat.ptr(ws), ws.numel(),
                                    nat.stream_handle()), "ente_radius_counts")

@@ -61,7 +61,11 @@ def test_workspace_sizes_are_host_only():
     assert n > 60000 * (8 * 4 + 16 * 4)
     assert L.ente_te_reduce_workspace_size(table, 2) >= 2 * 60000 * 8
     assert L.ente_jitter_workspace_size(2, 7) > 0
-    assert L.ente_radius_counts_workspace_size(2) > 0
+    table = nat.chunk_table([0, 10], [10, 20])
+    assert L.ente_radius_counts_workspace_size(table, 2, 7) > 0
+    assert L.ente_search_path(7, nat.masks_array([0b1110, 0b1111, 0b1111110]), 3, 4) == 1
+    assert L.ente_search_path(7, nat.masks_array([0b101]), 1, 4) == 2
+    assert L.ente_search_path(20, nat.masks_array([1]), 1, 4) == 0
 
 
 def test_chunk_struct_layout():

@@ -240,8 +240,9 @@ def test_split_search_parts_cover_every_row_once(parts):
     import torch
     from paper_1401_4068_b200.engine import search_device
     rng = np.random.default_rng(parts)
+    dup = np.repeat(rng.standard_normal((40, 7)), 6, axis=0)  # >= k+1 copies: eps == 0
     chunks = [rng.standard_normal((7000, 7)), np.round(rng.standard_normal((3000, 7)), 1),
-              rng.standard_normal((200, 7))]
+              rng.standard_normal((200, 7)), dup]
     ns = np.array([len(c) for c in chunks])
     rows0 = np.concatenate([[0], np.cumsum(ns)[:-1]])
     dev = torch.from_numpy(np.concatenate(chunks)).cuda()
@@ -251,11 +252,16 @@ def test_split_search_parts_cover_every_row_once(parts):
     cnt_sum = torch.zeros((3, dev.shape[0]), dtype=torch.int32, device=dev.device)
     written = torch.zeros(dev.shape[0], dtype=torch.int32, device=dev.device)
     for part in range(parts):
-        eps, cnt, _ = search_device(dev, rows0, ns, masks, 4, split=(part, parts))
-        eps_sum += eps
-        cnt_sum += cnt
-        written += (eps != 0).int()
-    assert int(written.max()) <= 1
+        # rows outside the part keep the fill: NaN / -1 mark them unwritten, so
+        # rows with eps == 0 (duplicates) still count as written
+        eps, cnt, _ = search_device(dev, rows0, ns, masks, 4, split=(part, parts),
+                                    split_fill=(float("nan"), -1))
+        mine = ~torch.isnan(eps)
+        assert bool((cnt[:, mine] >= 0).all()) and bool((cnt[:, ~mine] == -1).all())
+        eps_sum += torch.where(mine, eps, torch.zeros_like(eps))
+        cnt_sum += torch.where(mine[None, :], cnt, torch.zeros_like(cnt))
+        written += mine.int()
+    assert int(written.min()) == 1 and int(written.max()) == 1
     for c, r0, n in zip(chunks, rows0, ns):
         e, cnt = oracle.search(c, margs, 4)
         assert np.array_equal(eps_sum[r0:r0 + n].cpu().numpy(), e)
