@@ -459,7 +459,8 @@ def run_c3(args):
     e2e = None
     if not args.no_e2e:
         items = [(Chunk(p, chunk_id=i), margs) for i, p in enumerate(host)]
-        batch_search(items[:1], k)
+        for _ in range(min(2, args.warmup)):  # full-size: pinned result buffers are cached
+            batch_search(items, k)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):

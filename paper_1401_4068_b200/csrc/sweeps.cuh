@@ -44,6 +44,9 @@ constexpr int kGate = 4;                    // gate columns in the Morton key an
 #ifndef ENTE_CNT_UNROLL
 #define ENTE_CNT_UNROLL 2    // count pass: row-pair iterations unrolled per loop trip
 #endif
+#ifndef ENTE_KNN_V2
+#define ENTE_KNN_V2 0  // compacted kNN pass: straight-line row visit (no gate vote)
+#endif
 #ifndef ENTE_KNNC_UNROLL
 #define ENTE_KNNC_UNROLL 1   // compacted kNN pass: row-pair iterations per loop trip
 #endif
@@ -172,6 +175,22 @@ __device__ __forceinline__ Band make_band(float t32, double delta) {
     return b;
 }
 
+// lane index read once into a register the compiler cannot rematerialise:
+// with threadIdx.x it re-reads SR_TID (an S2R, ~20 cycles) inside the walk
+// loops whenever registers are tight
+#ifndef ENTE_PIN_LANE
+#define ENTE_PIN_LANE 1
+#endif
+__device__ __forceinline__ int pinned_lane() {
+#if ENTE_PIN_LANE
+    int l;
+    asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+    return l;
+#else
+    return threadIdx.x & 31;
+#endif
+}
+
 __device__ __forceinline__ float warp_max_nonneg(float v) {
     return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(v, 0.0f))));
 }
@@ -222,6 +241,7 @@ struct Walker {
     Box<Q> nb;      // its box
     Box<Q> own;     // the warp's own box, identical in all lanes
     uint32_t need;  // per lane: refs_need() bits of the sub-tile last returned
+    int ln;         // this lane
 
     __device__ int sub_at(int pos) const {
         if (pos < nh) return h0 + pos;
@@ -235,7 +255,8 @@ struct Walker {
         if (nst >= 0) nb = load_box<Q>(fb, nst);
     }
 
-    __device__ void init(const float4 *__restrict__ fb, int wrow, int n, int npad) {
+    __device__ void init(const float4 *__restrict__ fb, int wrow, int n, int npad, int lane) {
+        ln = lane;
         h0 = wrow / kSub;
         nh = (min(wrow + 32 * kRT, n) - wrow + kSub - 1) / kSub;
         nsub = npad / kSub;
@@ -253,7 +274,7 @@ struct Walker {
                                         fmaxf(own.hi[q].z, b.hi[q].z), fmaxf(own.hi[q].w, b.hi[q].w));
             }
         }
-        prefetch(fb, (threadIdx.x & 31));
+        prefetch(fb, ln);
     }
 
     // fp32 box distance (a lower bound of every d32 between the two boxes:
@@ -272,7 +293,7 @@ struct Walker {
     template <class RefTest>
     __device__ int next(const float4 *__restrict__ fb, float bound, bool strict,
                         RefTest &&refs_need) {
-        const int lane = threadIdx.x & 31;
+        const int lane = ln;
         for (;;) {
             while (mask == 0) {
                 if (base + 32 >= npos) return -1;
@@ -364,7 +385,7 @@ __global__ void __launch_bounds__(32, S > 16 ? 24 : (S > 8 ? 16 : sweep_minb(1 +
     const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
-    const int lane = threadIdx.x;
+    const int lane = pinned_lane();
     const float *cp = pts32 + ci.prow0 * DP;
     const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2 * kKnnQ;
     const int wrow = tr.r0;
@@ -401,7 +422,7 @@ __global__ void __launch_bounds__(32, S > 16 ? 24 : (S > 8 ? 16 : sweep_minb(1 +
     fence_barrier_init();
     __syncwarp();
     Walker<kKnnQ> wk;
-    wk.init(fb, wrow, ci.n, ci.npad);
+    wk.init(fb, wrow, ci.n, ci.npad, lane);
     float bound = INFINITY;  // warp max of the current k-th distances
     auto refs_need = [&](const Box<kKnnQ> &b) {
         bool need = !prune;
@@ -535,7 +556,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) kn
     const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
-    const int lane = threadIdx.x;
+    const int lane = pinned_lane();
     const unsigned lt = (1u << lane) - 1u;
     const float *cp = pts32 + ci.prow0 * DP;
     const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2 * kKnnQ;
@@ -598,7 +619,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) kn
     fence_barrier_init();
     __syncwarp();
     Walker<kKnnQ> wk;
-    wk.init(fb, wrow, ci.n, ci.npad);
+    wk.init(fb, wrow, ci.n, ci.npad, lane);
     float bound = INFINITY;  // warp max of the current k-th distances
     int slot_st = -1;
     uint32_t slot_need = 0u;
@@ -647,11 +668,16 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) kn
             auto visit = [&](const float4 (&cur)[NQ]) {
                 const float2 *c = reinterpret_cast<const float2 *>(cur);
                 float a[2 * NP];
+#if ENTE_KNN_V2
+                diff_pairs<D, 0, NP>(ref, c, a);
+                const float dj = maxabs0<0, D, 2 * NP>(a);
+#else
                 diff_pairs<D, 0, PG>(ref, c, a);
                 float dj = maxabs0<0, GC, 2 * NP>(a);
                 if (!__any_sync(0xffffffffu, dj < thr)) return;
                 diff_pairs<D, PG, NP>(ref, c, a);
                 dj = maxabs<GC, D, 2 * NP>(a, dj);
+#endif
                 if (dj < thr) {
                     insert_sorted<S>(kd, dj);
                     thr = fminf(thr, kd[S - 1]);
@@ -750,7 +776,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
     const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
-    const int lane = threadIdx.x;
+    const int lane = pinned_lane();
     const float *cp = pts32 + ci.prow0 * DP;
     const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2;
     const int wrow = tr.r0;
@@ -788,7 +814,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
     fence_barrier_init();
     __syncwarp();
     Walker<1> wk;
-    wk.init(fb, wrow, ci.n, ci.npad);
+    wk.init(fb, wrow, ci.n, ci.npad, lane);
     int slot_st = -1;
     int issued = 0;
     uint32_t nsub = 0;
@@ -922,7 +948,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
     const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     if (!ci.ok32) return;
-    const int lane = threadIdx.x;
+    const int lane = pinned_lane();
     const unsigned lt = (1u << lane) - 1u;
     const float *cp = pts32 + ci.prow0 * DP;
     const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2;
@@ -981,7 +1007,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
     fence_barrier_init();
     __syncwarp();
     Walker<1> wk;
-    wk.init(fb, wrow, ci.n, ci.npad);
+    wk.init(fb, wrow, ci.n, ci.npad, lane);
     int slot_st = -1;
     uint32_t slot_need = 0u;  // kRT bits per ring slot: this lane's needs of the issued sub-tiles
     int issued = 0;
