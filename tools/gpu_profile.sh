@@ -20,3 +20,8 @@ python tools/ncu_summary.py gpurun_out/${tag}_prof.ncu-rep > gpurun_out/${tag}_n
 python tools/ncu_summary.py gpurun_out/${tag}_prof.ncu-rep --traffic --merge profiles/ncu_traffic.json --config $cfg > gpurun_out/${tag}_ncu_traffic.json 2>&1
 cp profiles/ncu_traffic.json gpurun_out/${tag}_ncu_traffic_all.json
 cat gpurun_out/${tag}_ncu_traffic.json
+# instruction mix / hot lines of the two sweeps (text), then drop the report
+# unless KEEP_REP=1 (gpurun copies back at most 64 MiB)
+python tools/ncu_hot.py gpurun_out/${tag}_prof.ncu-rep count_pass > gpurun_out/${tag}_count_mix.txt 2>&1
+python tools/ncu_hot.py gpurun_out/${tag}_prof.ncu-rep knn > gpurun_out/${tag}_knn_mix.txt 2>&1
+if [ "${KEEP_REP:-0}" != "1" ]; then rm -f gpurun_out/${tag}_prof.ncu-rep; fi
