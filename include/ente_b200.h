@@ -168,6 +168,33 @@ int ente_radius_counts(const double *pts64, int64_t total_rows, int dim, const e
 int ente_search_path(int dim, const uint32_t *marg_masks, int n_marg, int k);
 
 /* ---------------------------------------------------------------------------
+ * ente_search_te_shared -- ente_search for a TE batch whose chunks all pool
+ * the same target rows (r, t) of one window: chunk c's row r * w + t takes
+ * its y columns (y_t, y-past) from repetition perms[chunk_perm[c]][r]
+ * (identity for chunk_perm[c] = -1) -- every (u, surrogate) chunk of one
+ * analyze_pair window.  Same outputs as ente_search with the three TE
+ * marginals; the two y marginals are counted once per original point for the
+ * whole batch (shared_y.cuh), the joint / y-past + x-past ones by the sweeps.
+ * Falls back to ente_search when the batch does not qualify.
+ *
+ * Replaces: ente.ksg.estimate_te_batch's batch_search call (ksg.py:83) for the
+ *           bundles of analyze_pair (inference.py:147,173)
+ *
+ *   y0           [dev]  [reps * w x (1 + dy)] fp64 unjittered y columns, row p = r * w + t
+ *   chunk_perm   [host] n_chunks surrogate indices (-1 = original data)
+ *   perms, inv_perms [dev] [n_perm x reps] int32 permutations and their inverses
+ *   margin       >= |D_c(p, q) - D0(p, q)| for every chunk c: 2 x the jitter
+ *                half width (amplitude x std) plus rounding (host computes it)
+ * ------------------------------------------------------------------------- */
+size_t ente_search_te_shared_workspace_size(const ente_chunk *chunks, int n_chunks, int dim, int dy,
+                                            int k);
+int ente_search_te_shared(const double *pts64, int64_t total_rows, int dim, const ente_chunk *chunks,
+                          int n_chunks, int dy, int k, const double *y0, int reps, int w,
+                          const int32_t *chunk_perm, const int32_t *perms, const int32_t *inv_perms,
+                          double margin, double *out_eps, int32_t *out_counts, int32_t *status,
+                          void *workspace, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
  * ente_jitter -- tie-breaking jitter, in place:
  *   pts += U(-1, 1) * (amplitude * std(pts, axis=0))     per chunk
  * with numpy's exact arithmetic: column std as a sequential row-order sum

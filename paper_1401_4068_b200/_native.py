@@ -51,6 +51,9 @@ def _declare(L):
                                vp], i32),
         "ente_radius_counts_workspace_size": ([cp, i32, i32], sz),
         "ente_search_path": ([i32, u32p, i32, i32], i32),
+        "ente_search_te_shared_workspace_size": ([cp, i32, i32, i32, i32], sz),
+        "ente_search_te_shared": ([vp, i64, i32, cp, i32, i32, i32, vp, i32, i32, i32p, vp, vp, dbl,
+                                   vp, vp, vp, vp, sz, vp], i32),
         "ente_radius_counts": ([vp, i64, i32, cp, i32, u32p, i32, vp, vp, vp, vp, sz, vp], i32),
         "ente_jitter_workspace_size": ([i32, i32], sz),
         "ente_jitter": ([vp, i32, cp, i32, u64p, dbl, vp, vp, sz, vp], i32),

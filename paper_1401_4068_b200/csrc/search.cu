@@ -41,6 +41,7 @@
 #include "common.cuh"
 #include "profile.cuh"
 #include "radix.cuh"
+#include "shared_y.cuh"
 #include "sweeps.cuh"
 
 namespace ente {
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(kTJ) gather_knn_kernel(
         const bool valid = s < ci.n;
         const int32_t o = valid ? permk[ci.row0 + s] : 0;
         const int64_t orig = ci.row0 + o;
-        if (valid) kmap[ci.row0 + s] = inv[orig];
+        if (valid && kmap) kmap[ci.row0 + s] = inv[orig];
         float4 *q4 = reinterpret_cast<float4 *>(pts32 + (ci.prow0 + s) * dp);
         float4 quad = make_float4(0.f, 0.f, 0.f, 0.f);
         const int64_t sub = ci.prow0 / kSub + stage * (kTJ / kSub) + warp * (32 / kSub) + lane / kSub;
@@ -560,7 +561,8 @@ __global__ void __launch_bounds__(kWarpRefs) resolve_kernel(
     const uint32_t *__restrict__ ev, const int32_t *__restrict__ ev_n, int64_t ws_rows,
     int64_t total_rows, double *__restrict__ out_eps, int32_t *__restrict__ out_counts,
     int64_t *__restrict__ ovf_list, int32_t *__restrict__ ovf_n, int64_t *__restrict__ rs_list,
-    int32_t *__restrict__ rs_n, int32_t *__restrict__ rs_flag) {
+    int32_t *__restrict__ rs_n, int32_t *__restrict__ rs_flag, int allow_rescan,
+    uint32_t *__restrict__ kstar) {
     const TileRef tr = tile_of(tile0, n_chunks, blockIdx.x);
     const ChunkInfo ci = info[tr.chunk];
     const int s = tr.r0 + threadIdx.x;  // sorted position
@@ -577,6 +579,7 @@ __global__ void __launch_bounds__(kWarpRefs) resolve_kernel(
         const double *rp = pts64 + row * dim;
         for (int c = 0; c < dim; ++c) ref[c] = rp[c];
         double dj[kCap];
+        int jj[kCap];
         int nj = 0;
         for (int e = 0; e < ne; ++e) {
             const uint32_t w = ev[srow * kCap + e];
@@ -587,14 +590,22 @@ __global__ void __launch_bounds__(kWarpRefs) resolve_kernel(
             int p = nj++;
             while (p > 0 && dj[p - 1] > jd) {
                 dj[p] = dj[p - 1];
+                jj[p] = jj[p - 1];
                 --p;
             }
             dj[p] = jd;
+            jj[p] = j;
         }
         if (need > nj) {
             fallback = true;
         } else {
             eps = dj[need - 1];
+            if (kstar) {  // a neighbour at exactly eps, with its y-marginal verdicts (shared-y)
+                const int qrow = perm[ci.row0 + jj[need - 1]];
+                double A, m2, m3, jd;
+                te_dist64(ref, pts64 + (ci.row0 + qrow) * dim, dim, lay.dy, A, m2, m3, jd);
+                kstar[row] = (uint32_t)qrow | ((A < eps) ? 1u << 30 : 0u) | ((m2 < eps) ? 1u << 31 : 0u);
+            }
             for (int e = 0; e < ne; ++e) {
                 const uint32_t w = ev[srow * kCap + e];
                 const int j = (int)(w & 0x0FFFFFFFu);
@@ -609,7 +620,8 @@ __global__ void __launch_bounds__(kWarpRefs) resolve_kernel(
         }
     }
     if (fallback) {
-        if (ci.ok32) {  // fp32 data usable: pruned warp rescan of the sorted row
+        if (kstar) kstar[row] = 0xFFFFFFFFu;
+        if (ci.ok32 && allow_rescan) {  // fp32 data usable: pruned warp rescan of the sorted row
             const int slot = atomicAdd(rs_n, 1);
             rs_list[slot] = srow;
             rs_flag[tr.chunk] = 1;
@@ -1133,7 +1145,7 @@ static int validate(const ente_chunk *chunks, int n_chunks, int dim, const uint3
 // prep -> principal axes -> both sort orders -> both fp32 copies with boxes
 static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Plan &p,
                          const SearchWs &w, int n_chunks, int32_t *status, int prune,
-                         int allow_pca = 1, bool count_only = false) {
+                         int allow_pca = 1, bool count_only = false, bool knn_only = false) {
         ENTE_LAUNCH("prep", st,
                     (p.max_npad <= kPrepSmallN ? prep_kernel<kPrepThreadsSmall> : prep_kernel<kPrepThreadsBig>)
                     <<<n_chunks, p.max_npad <= kPrepSmallN ? kPrepThreadsSmall : kPrepThreadsBig, 0, st>>>(
@@ -1168,15 +1180,17 @@ static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Pl
                                                                        w.perm, w.permk));
         ENTE_CUDA(cudaGetLastError());
         dim3 ggrid((unsigned)(p.max_npad / kTJ), (unsigned)std::min(n_chunks, 65535));
-        ENTE_LAUNCH("gather", st,
-                    gather_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.stats,
-                                                         w.perm, p.dp, p.fc, w.pts32, w.fbox,
-                                                         w.inv));
-        ENTE_CUDA(cudaGetLastError());
+        if (!knn_only) {  // (shared-y batches sweep the kNN order only: no count-order copy)
+            ENTE_LAUNCH("gather", st,
+                        gather_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.stats,
+                                                             w.perm, p.dp, p.fc, w.pts32, w.fbox,
+                                                             w.inv));
+            ENTE_CUDA(cudaGetLastError());
+        }
         ENTE_LAUNCH("gather_knn", st,
                     gather_knn_kernel<<<ggrid, kTJ, 0, st>>>(pts64, dim, w.info, n_chunks, w.stats,
                                                              w.permk, w.inv, p.dp, w.pts32k,
-                                                             w.fboxk, w.kmap));
+                                                             w.fboxk, knn_only ? nullptr : w.kmap));
         ENTE_CUDA(cudaGetLastError());
     return ENTE_OK;
 }
@@ -1561,7 +1575,7 @@ static int search_impl(const double *pts64, int64_t total_rows, int dim, const e
                     resolve_kernel<<<nt, kWarpRefs, 0, st>>>(pts64, dim, w.info, w.tile0, n_chunks, k, p.lay,
                                                        w.perm, w.L, w.cnt3, w.ev, w.ev_n, ws_rows,
                                                        total_rows, out_eps, out_counts, w.ovf,
-                                                       w.ovf_n, w.rs, w.rs_n, w.rs_flag));
+                                                       w.ovf_n, w.rs, w.rs_n, w.rs_flag, 1, nullptr));
         ENTE_CUDA(cudaGetLastError());
         {
             dim3 ggrid((unsigned)(p.max_npad / kTJ), (unsigned)std::min(n_chunks, 65535));
@@ -1611,6 +1625,199 @@ extern "C" int ente_search_split(const double *pts64, int64_t total_rows, int di
     }
     return search_impl(pts64, total_rows, dim, chunks, n_chunks, marg_masks, n_marg, k, out_eps,
                        out_counts, status, workspace, ws_bytes, stream, split_index, split_count);
+}
+
+// ---------------------------------------------------------------------------
+// Shared-y TE batches (shared_y.cuh): the kNN sweep, an m3 + joint-band sweep
+// over the kNN order, fp64 resolve, and the y-marginal counts once per
+// original point for the whole batch.
+// ---------------------------------------------------------------------------
+struct SyBufs {
+    int32_t *chunk_perm, *va, *vb, *parity, *yva, *yvb, *yperm;
+    uint32_t *ka, *kb, *kstar, *qs;
+    uint32_t *yka, *ykb;
+    double *ys, *box;
+};
+
+static size_t sy_smem_bytes(int C, int nsub) {
+    return (size_t)C * 4 * 3 + 2 * (size_t)(C + 1) * 4 + 2 * (size_t)C * 4 + (size_t)kSyBins * 4 +
+           (size_t)nsub * 4;
+}
+
+static SyBufs sy_layout(Arena &a, int64_t m, int C, int dd) {
+    SyBufs b{};
+    const int nsub = (int)((m + 31) / 32);
+    b.chunk_perm = a.take<int32_t>(C);
+    b.ka = a.take<uint32_t>((size_t)m * C);
+    b.kb = a.take<uint32_t>((size_t)m * C);
+    b.va = a.take<int32_t>((size_t)m * C);
+    b.vb = a.take<int32_t>((size_t)m * C);
+    b.qs = a.take<uint32_t>((size_t)m * C);
+    b.kstar = a.take<uint32_t>((size_t)m * C);
+    b.parity = a.take<int32_t>(m);
+    b.yka = a.take<uint32_t>(m);
+    b.ykb = a.take<uint32_t>(m);
+    b.yva = a.take<int32_t>(m);
+    b.yvb = a.take<int32_t>(m);
+    b.yperm = a.take<int32_t>(m);
+    b.ys = a.take<double>((size_t)m * dd);
+    b.box = a.take<double>((size_t)nsub * 2 * (dd - 1));
+    return b;
+}
+
+static bool sy_usable(const Plan &p, int n_chunks, int64_t m, int k) {
+    SweepSet ss;
+    return p.fast && p.lay.nout == 3 && p.lay.slot[0] == 0 && p.lay.slot[1] == 1 && p.lay.slot[2] == 2 &&
+           p.max_npad >= kCompactMinRows && k + 1 <= 16 && find_sweep_set(p.dy, p.dx, ss) &&
+           ss.count3 != nullptr && 1 + p.dy <= kSyMaxY &&
+           sy_smem_bytes(n_chunks, (int)((m + 31) / 32)) <= 200 * 1024;
+}
+
+static void te_masks_of(int dy, int dim, uint32_t *masks) {
+    masks[0] = ((1u << (dy + 1)) - 1u) & ~1u;                          // y-past
+    masks[1] = (1u << (dy + 1)) - 1u;                                   // y_t + y-past
+    masks[2] = ((dim >= 32) ? 0xFFFFFFFFu : ((1u << dim) - 1u)) & ~1u;  // y-past + x-past
+}
+
+extern "C" size_t ente_search_te_shared_workspace_size(const ente_chunk *chunks, int n_chunks, int dim,
+                                                       int dy, int k) {
+    uint32_t masks[3];
+    te_masks_of(dy, dim, masks);
+    Plan p = make_plan(chunks, n_chunks, dim, masks, 3, k);
+    if (!p.fast) return ente_search_workspace_size(chunks, n_chunks, dim, 3, k);
+    Arena a(nullptr, 0);
+    layout_ws(a, p, n_chunks);
+    const int64_t m = n_chunks > 0 ? chunks[0].n : 0;
+    sy_layout(a, m, n_chunks, 1 + dy);
+    return std::max(a.used, ente_search_workspace_size(chunks, n_chunks, dim, 3, k)) + 256;
+}
+
+extern "C" int ente_search_te_shared(const double *pts64, int64_t total_rows, int dim,
+                                     const ente_chunk *chunks, int n_chunks, int dy, int k,
+                                     const double *y0, int reps, int w, const int32_t *chunk_perm,
+                                     const int32_t *perms, const int32_t *inv_perms, double margin,
+                                     double *out_eps, int32_t *out_counts, int32_t *status,
+                                     void *workspace, size_t ws_bytes, void *stream) {
+    if (dy < 1 || dim - 1 - dy < 0 || reps < 1 || w < 1 || !y0 || !chunk_perm || !(margin >= 0.0)) {
+        set_error("ente_search_te_shared: bad arguments");
+        return ENTE_ERR_ARG;
+    }
+    uint32_t masks[3];
+    te_masks_of(dy, dim, masks);
+    int rc = validate(chunks, n_chunks, dim, masks, 3, k);
+    if (rc != ENTE_OK) return rc;
+    if (n_chunks == 0) return ENTE_OK;
+    const int64_t m = (int64_t)reps * w;
+    for (int c = 0; c < n_chunks; ++c)
+        if (chunks[c].n != m) {
+            set_error("ente_search_te_shared: chunk %d has %d rows, expected reps * w = %lld", c,
+                      chunks[c].n, (long long)m);
+            return ENTE_ERR_ARG;
+        }
+    Plan p = make_plan(chunks, n_chunks, dim, masks, 3, k);
+    if (!sy_usable(p, n_chunks, m, k))  // the general search gives the same counts
+        return search_impl(pts64, total_rows, dim, chunks, n_chunks, masks, 3, k, out_eps, out_counts,
+                           status, workspace, ws_bytes, stream, 0, 1);
+    if (p.total_rows > total_rows) {
+        set_error("ente_search_te_shared: chunks reference rows beyond total_rows");
+        return ENTE_ERR_ARG;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t ws_rows = p.total_rows;
+    Arena a(workspace, ws_bytes);
+    SearchWs w_ = layout_ws(a, p, n_chunks);
+    SyBufs b = sy_layout(a, m, n_chunks, 1 + dy);
+    if (!a.ok() || !w_.info || !b.box) {
+        set_error("ente_search_te_shared: workspace of %zu bytes too small (need %zu)", ws_bytes, a.used);
+        return ENTE_ERR_WORKSPACE;
+    }
+    std::vector<int32_t> htile0;
+    int32_t ntiles = 0;
+    rc = upload_chunks(st, chunks, n_chunks, k, p, w_, status, htile0, ntiles);
+    if (rc != ENTE_OK) return rc;
+    const int prune = prune_enabled();
+    unsigned long long *work = device_work();
+    if (!work) {
+        set_error("ente_search_te_shared: cannot allocate the work counters");
+        return ENTE_ERR_CUDA;
+    }
+    rc = launch_orders(st, pts64, dim, p, w_, n_chunks, status, prune, 1, false, true);
+    if (rc != ENTE_OK) return rc;
+    ENTE_CUDA(cudaMemcpyAsync(w_.tile0, htile0.data(), sizeof(int32_t) * (2 * n_chunks + 1),
+                              cudaMemcpyHostToDevice, st));
+    ENTE_CUDA(cudaMemcpyAsync(b.chunk_perm, chunk_perm, sizeof(int32_t) * n_chunks,
+                              cudaMemcpyHostToDevice, st));
+    SweepSet ss;
+    find_sweep_set(p.dy, p.dx, ss);
+    if (ntiles > 0) {
+        const unsigned nt = (unsigned)ntiles;
+        const KnnFn knn_fn = knn_table(p.dy, p.dx, p.slots, p.max_npad);
+        prefer_shared(reinterpret_cast<const void *>(knn_fn));
+        prefer_shared(reinterpret_cast<const void *>(ss.count3));
+        ENTE_LAUNCH("knn_pass", st,
+                    knn_fn<<<nt, 32, 0, st>>>(w_.pts32k, w_.fboxk, w_.info, w_.tile0, n_chunks, k, prune,
+                                              nullptr, w_.t32, w_.L, work));
+        ENTE_CUDA(cudaGetLastError());
+        ENTE_LAUNCH("count_pass", st,
+                    ss.count3<<<nt, 32, 0, st>>>(w_.pts32k, w_.fboxk, w_.info, w_.tile0, n_chunks, w_.t32,
+                                                 ws_rows, prune, w_.cnt3, w_.ev, w_.ev_n, 4u | 8u,
+                                                 work + 1));
+        ENTE_CUDA(cudaGetLastError());
+        ENTE_LAUNCH("resolve", st,
+                    resolve_kernel<<<nt, kWarpRefs, 0, st>>>(pts64, dim, w_.info, w_.tile0, n_chunks, k,
+                                                             p.lay, w_.permk, w_.L, w_.cnt3, w_.ev,
+                                                             w_.ev_n, ws_rows, total_rows, out_eps,
+                                                             out_counts, w_.ovf, w_.ovf_n, w_.rs,
+                                                             w_.rs_n, w_.rs_flag, 0, b.kstar));
+        ENTE_CUDA(cudaGetLastError());
+    }
+    Masks mk{};
+    mk.n = 3;
+    for (int i = 0; i < 3; ++i) mk.m[i] = masks[i];
+    dispatch_exact(k, st, pts64, dim, w_.info, n_chunks, status, w_.ovf, w_.ovf_n, 0, mk, total_rows,
+                   out_eps, out_counts);
+    ENTE_CUDA(cudaGetLastError());
+    // y-marginal counts once per original point
+    SyGeom g;
+    g.reps = reps;
+    g.w = w;
+    g.m = (int)m;
+    g.C = n_chunks;
+    g.dd = 1 + dy;
+    g.nsub = (int)((m + 31) / 32);
+    g.margin = margin;
+    {
+        dim3 grid((unsigned)std::min<int64_t>((m + 255) / 256, 1024), (unsigned)n_chunks);
+        ENTE_LAUNCH("sy_scatter", st,
+                    sy_scatter_kernel<<<grid, 256, 0, st>>>(w_.info, b.chunk_perm, perms, g, out_eps,
+                                                             b.kstar, b.ka, b.va, b.qs));
+        ENTE_CUDA(cudaGetLastError());
+    }
+    if (n_chunks <= kSortSmallN) {
+        ENTE_LAUNCH("sy_sort", st,
+                    sy_sort_kernel<kSortThreadsSmall><<<(unsigned)m, kSortThreadsSmall, 0, st>>>(
+                        b.ka, b.kb, b.va, b.vb, n_chunks, b.parity));
+    } else {
+        ENTE_LAUNCH("sy_sort", st,
+                    sy_sort_kernel<kSortThreads><<<(unsigned)m, kSortThreads, 0, st>>>(
+                        b.ka, b.kb, b.va, b.vb, n_chunks, b.parity));
+    }
+    ENTE_CUDA(cudaGetLastError());
+    ENTE_LAUNCH("sy_order", st,
+                sy_order_kernel<<<1, kSortThreads, 0, st>>>(y0, g, b.yka, b.ykb, b.yva, b.yvb, b.yperm));
+    ENTE_CUDA(cudaGetLastError());
+    ENTE_LAUNCH("sy_gather", st,
+                sy_gather_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(y0, g, b.yperm, b.ys, b.box));
+    ENTE_CUDA(cudaGetLastError());
+    const size_t smem = sy_smem_bytes(n_chunks, g.nsub);
+    ENTE_CUDA(cudaFuncSetAttribute(sy_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    ENTE_LAUNCH("sy_count", st,
+                sy_count_kernel<<<(unsigned)m, kSyThreads, smem, st>>>(
+                    y0, b.ys, b.yperm, b.box, g, b.ka, b.kb, b.va, b.vb, b.qs, b.parity, w_.info, b.chunk_perm,
+                    inv_perms, pts64, dim, out_eps, total_rows, out_counts));
+    ENTE_CUDA(cudaGetLastError());
+    return ENTE_OK;
 }
 
 // Evaluated (reference, candidate) pairs of the two sweeps on the current

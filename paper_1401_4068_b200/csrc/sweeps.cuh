@@ -335,6 +335,23 @@ __device__ __forceinline__ float point_box(const float2 (&nr)[NP], const Box<Q> 
     return d;
 }
 
+// the same lower bound over columns C0 .. C1-1 of a box whose slot g holds
+// column g (the kNN-order boxes, columns 0 .. 4Q-1)
+template <int C0, int C1, int NP, int Q>
+__device__ __forceinline__ float point_box_cols(const float2 (&nr)[NP], const Box<Q> &b) {
+    float d = 0.0f;
+#pragma unroll
+    for (int c = C0; c < C1; ++c) {
+        const float x = (c & 1) ? nr[c >> 1].y : nr[c >> 1].x;  // -x_c
+        const float4 l4 = b.lo[c >> 2], h4 = b.hi[c >> 2];
+        const float l = (c & 3) == 0 ? l4.x : (c & 3) == 1 ? l4.y : (c & 3) == 2 ? l4.z : l4.w;
+        const float h = (c & 3) == 0 ? h4.x : (c & 3) == 1 ? h4.y : (c & 3) == 2 ? h4.z : h4.w;
+        const float2 e = __fadd2_rn(make_float2(l, h), make_float2(x, x));
+        d = fmaxf(fmaxf(d, e.x), -e.y);
+    }
+    return d;
+}
+
 template <int DP, int NSLOT>
 struct Ring {
     float buf[NSLOT][kSub * DP];
@@ -924,7 +941,12 @@ struct CountRefs {
     int slot[32 * kRT];       // compacted reference list of the current sub-tile
 };
 
-template <int DY, int DX>
+// KO (shared-y TE batches): the same sweep over the kNN-order copy and its
+// all-column boxes, counting only the y-past + x-past marginal (m3) and
+// recording m3 / joint (jd) band events; the y marginals are counted once
+// per point for the whole batch (shared_y.cu).  Pruning uses box columns
+// 1 .. 4*kKnnQ-1 (column 0 is not in m3, which bounds jd from below).
+template <int DY, int DX, bool KO>
 __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) count_pass_kernel(
     const float *__restrict__ pts32, const float *__restrict__ fbox,
     const ChunkInfo *__restrict__ info, const int32_t *__restrict__ tile0, int n_chunks,
@@ -943,7 +965,8 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
     const int lane = pinned_lane();
     const unsigned lt = (1u << lane) - 1u;
     const float *cp = pts32 + ci.prow0 * DP;
-    const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2;
+    constexpr int Q = KO ? kKnnQ : 1;  // float4 quads per box half
+    const float4 *fb = reinterpret_cast<const float4 *>(fbox) + (ci.prow0 / kSub) * 2 * Q;
     const int wrow = tr.r0;
     float myhi[kRT];
     float hmax = 0.0f;
@@ -972,6 +995,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
     }
     const float bound = warp_max_nonneg(hmax);
     constexpr int NG = DY < kGate ? DY : kGate;
+    constexpr int NBC = D < 4 * kKnnQ ? D : 4 * kKnnQ;  // KO: box columns 0 .. NBC-1
     // this lane's own references' gate columns (negated, packed), read back
     // from shared memory so they hold no registers through the rounds
     struct NegRef {
@@ -982,24 +1006,31 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
         const float2 *rr = reinterpret_cast<const float2 *>(rs.ref[r * 32 + lane]);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            const float2 v = p <= NG / 2 ? rr[p] : make_float2(0.0f, 0.0f);
+            const float2 v = (KO || p <= NG / 2) ? rr[p] : make_float2(0.0f, 0.0f);
             nr.v[p] = make_float2(-v.x, -v.y);
         }
         return nr;
     };
-    auto refs_need = [&](const Box<1> &b) {
+    auto refs_need = [&](const Box<Q> &b) {
         uint32_t need = 0u;
 #pragma unroll
-        for (int r = 0; r < kRT; ++r)
-            need |= ((!prune && myhi[r] > -INFINITY) || point_box<1, NG, NP, 1>(gate_ref(r).v, b) <= myhi[r])
-                        ? (1u << r) : 0u;
+        for (int r = 0; r < kRT; ++r) {
+            float d;
+            if constexpr (KO) d = point_box_cols<1, NBC, NP, Q>(gate_ref(r).v, b);
+            else d = point_box<1, NG, NP, 1>(gate_ref(r).v, b);
+            need |= ((!prune && myhi[r] > -INFINITY) || d <= myhi[r]) ? (1u << r) : 0u;
+        }
         return need;
     };
     if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
     fence_barrier_init();
     __syncwarp();
-    Walker<1> wk;
+    Walker<Q> wk;
     wk.init(fb, wrow, ci.n, ci.npad, lane);
+    if constexpr (KO) {  // column 0 is not an m3 column: the warp box spans it
+        wk.own.lo[0].x = -INFINITY;
+        wk.own.hi[0].x = INFINITY;
+    }
     int slot_st = -1;
     uint32_t slot_need = 0u;  // kRT bits per ring slot: this lane's needs of the issued sub-tiles
     int issued = 0;
@@ -1065,6 +1096,22 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
                 // are differenced unconditionally.  jd = max(m2, m3) is one
                 // of m2, m3, so the band test needs only A, m2, m3.
                 diff_pairs<D, 0, NP>(ref, c, a);
+                if constexpr (KO) {
+                    const float m3 = maxabs0<1, D, 2 * NP>(a);
+                    const float jd = fmaxf(m3, fabsf(a[0]));
+                    const float2 e = __fadd2_rn(make_float2(m3, jd), make_float2(nlo, nlo));
+                    c3 += __float_as_uint(e.x) >> 31;
+                    if (fminf(fabsf(e.x), fabsf(e.y)) <= wb) {
+                        uint32_t f = ((m3 >= lo && m3 <= hi) ? 4u : 0u) | ((jd >= lo && jd <= hi) ? 8u : 0u);
+                        f &= fmask;
+                        if (f) {
+                            const int pos = atomicAdd(&rs.nev[ri], 1);
+                            if (pos < kCap)
+                                ev[(ci.row0 + wrow + ri) * kCap + pos] = (uint32_t)(cur_st * kSub + j) | (f << 28);
+                        }
+                    }
+                    return;
+                }
                 const float A = maxabs0<1, 1 + DY, 2 * NP>(a);
                 const float m2 = fmaxf(A, fabsf(a[0]));
                 const float m3 = maxabs<1 + DY, D, 2 * NP>(a, A);
@@ -1146,8 +1193,8 @@ ENTE_UNROLL(ENTE_CNT_UNROLL)
         if (idx >= ci.n) continue;
         const uint32_t self = rs.lo[ri] > 0.0f ? 1u : 0u;  // the self pair counted as inside
         const int64_t row = ci.row0 + idx;
-        cnt_out[row] = (int32_t)(rs.cnt[0][ri] - self);
-        cnt_out[ws_rows + row] = (int32_t)(rs.cnt[1][ri] - self);
+        cnt_out[row] = KO ? 0 : (int32_t)(rs.cnt[0][ri] - self);
+        cnt_out[ws_rows + row] = KO ? 0 : (int32_t)(rs.cnt[1][ri] - self);
         cnt_out[2 * ws_rows + row] = (int32_t)(rs.cnt[2][ri] - self);
         ev_n[row] = rs.nev[ri];
     }
@@ -1344,6 +1391,7 @@ struct SweepSet {
     KnnFn knn_compact[3];  // k + 1 <= 5, 8, 16, compacted references (chunks >= 4096 rows)
     CountFn compact;   // count pass, compacted references (chunks >= 4096 rows)
     CountFn direct;    // count pass, two references per lane (small chunks)
+    CountFn count3;    // shared-y batches: m3 counts + m3/jd events on the kNN order (compacted)
     RescanFn rescan[5];  // k <= 4, 8, 16, 32, 64
 };
 
@@ -1358,7 +1406,8 @@ SweepSet make_sweep_set() {
     s.knn_compact[0] = knn_compact_kernel<DY, DX, 5>;
     s.knn_compact[1] = knn_compact_kernel<DY, DX, 8>;
     s.knn_compact[2] = knn_compact_kernel<DY, DX, 16>;
-    s.compact = count_pass_kernel<DY, DX>;
+    s.compact = count_pass_kernel<DY, DX, false>;
+    s.count3 = count_pass_kernel<DY, DX, true>;
     s.direct = count_pass_direct_kernel<DY, DX>;
     s.rescan[0] = rescan_kernel<DY, DX, 4>;
     s.rescan[1] = rescan_kernel<DY, DX, 8>;

@@ -144,6 +144,43 @@ def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int, reuse: bool = F
     return eps, counts[:len(masks)], status[:len(ns)]
 
 
+@dataclass(frozen=True)
+class SharedY:
+    """The common target point set of a TE batch (ente_search_te_shared):
+    y0 [reps * w, 1 + d_y] unjittered y columns on the device, every chunk's
+    surrogate index (-1 = original), the permutation tables (and inverses)
+    on the device, and the jitter margin."""
+
+    y0: torch.Tensor
+    reps: int
+    w: int
+    chunk_perm: np.ndarray
+    perms: torch.Tensor
+    inv_perms: torch.Tensor
+    margin: float
+
+
+def search_te_shared_device(pts64: torch.Tensor, rows0, ns, d_y: int, k: int, shared: SharedY,
+                            tag: str = ""):
+    """ente_search_te_shared on device-resident TE chunks: (eps, counts [3, rows], status)."""
+    rows, dim = pts64.shape
+    L = nat.lib()
+    table = nat.chunk_table(rows0, ns)
+    eps = nat.scratch("search.eps" + tag, (rows,), torch.float64)
+    counts = nat.scratch("search.counts" + tag, (3, rows), torch.int32)
+    status = nat.scratch("search.status" + tag, (max(1, len(ns)),), torch.int32)
+    need = L.ente_search_te_shared_workspace_size(table, len(ns), dim, int(d_y), int(k))
+    ws = nat.workspace(need, tag)
+    cp = np.ascontiguousarray(shared.chunk_perm, dtype=np.int32)
+    nat.check(L.ente_search_te_shared(
+        nat.ptr(pts64), rows, dim, table, len(ns), int(d_y), int(k), nat.ptr(shared.y0),
+        int(shared.reps), int(shared.w), cp.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+        nat.ptr(shared.perms), nat.ptr(shared.inv_perms), float(shared.margin), nat.ptr(eps),
+        nat.ptr(counts), nat.ptr(status), nat.ptr(ws), ws.numel(), nat.stream_handle()),
+        "ente_search_te_shared")
+    return eps, counts, status[:len(ns)]
+
+
 class _Pinned(threading.local):
     buf = None
 

@@ -26,6 +26,7 @@ from . import _native as nat
 from . import seeds
 from .data import AnalysisConfig, EnsembleSeries, TEResult, validate_ensemble
 from .embedding import EmbeddingSpec, PointSetBundle, check_assembly
+from .engine import SharedY
 from .exceptions import EnteError, InvalidPermutation, KTooLarge, UnknownMethod
 from .ksg import _raise_status, te_chunks_device
 
@@ -34,6 +35,9 @@ MAX_ROWS_PER_WAVE = 1 << 27
 # a wave runs as up to SUB_BATCHES sub-batches on two streams (>= MIN_SUB_BATCH chunks each)
 SUB_BATCHES = int(os.environ.get("ENTE_SUB_BATCHES", "1"))
 MIN_SUB_BATCH = 64
+# batches of one window count the y marginals once per target point
+# (ente_search_te_shared); ENTE_SHARED_Y=0 sweeps every chunk (A/B, tests)
+SHARED_Y = os.environ.get("ENTE_SHARED_Y", "1") != "0"
 
 
 @dataclass(frozen=True)
@@ -161,12 +165,42 @@ class PairPipeline:
         self.y = y_device if y_device is not None else \
             torch.from_numpy(np.array(target.values, dtype=np.float64)).to(dev)
         self.perm_dev = None
+        self.inv_perm_dev = None
         self.perm_count = 0
+        self.target_values = np.asarray(target.values, dtype=np.float64)
+        self._shared = {}
 
     def set_perms(self, perms):
         arr = np.ascontiguousarray(np.asarray(perms, dtype=np.int32).reshape(-1, self.reps))
         self.perm_dev = torch.from_numpy(arr).to(nat.device())
+        inv = np.empty_like(arr)
+        np.put_along_axis(inv, arr.astype(np.int64), np.arange(self.reps, dtype=np.int32)[None, :], 1)
+        self.inv_perm_dev = torch.from_numpy(np.ascontiguousarray(inv)).to(nat.device())
         self.perm_count = len(perms)
+        self._shared.clear()
+
+    def shared_y(self, t_lo: int, perm_index):
+        """SharedY of the window starting at t_lo (every chunk of the window
+        pools the same target rows): the unjittered y columns
+        (embedding.py:109-113) and the jitter margin 2 hw + rounding, hw =
+        amplitude x the columns' std (ksg.py:52-59)."""
+        hit = self._shared.get(t_lo)
+        if hit is None:
+            yv = self.target_values
+            times = np.arange(t_lo, t_lo + self.w)
+            cols = [yv[:, times - 1]] + [yv[:, times - 2 - j * self.sy.delay] for j in range(self.sy.dim)]
+            y0 = np.ascontiguousarray(np.stack([c.reshape(-1) for c in cols], axis=1))
+            hw = self.cfg.jitter_amplitude * float(y0.std(axis=0).max()) * (1.0 + 1e-9)
+            margin = 2.0 * hw * (1.0 + 1e-12) + 2.0 ** -48 * (float(np.abs(y0).max()) + hw)
+            hit = (torch.from_numpy(y0).to(nat.device()), margin)
+            self._shared[t_lo] = hit
+        y0, margin = hit
+        if self.perm_dev is None:
+            perms = inv = torch.zeros((1, self.reps), dtype=torch.int32, device=nat.device())
+        else:
+            perms, inv = self.perm_dev, self.inv_perm_dev
+        return SharedY(y0, self.reps, self.w, np.asarray(perm_index, dtype=np.int32), perms, inv,
+                       margin)
 
     def seed_tuple(self, u, perm_index):
         return (self.cfg.seed, u, 0 if perm_index < 0 else perm_index + 1)
@@ -248,9 +282,12 @@ class PairPipeline:
                   "ente_pack_te_items")
         rows0 = np.arange(n, dtype=np.int64) * self.m
         ns = np.full(n, self.m, dtype=np.int64)
+        shared = None
+        if SHARED_Y and (it[:, 2] == it[0, 2]).all():  # one window: one target point set
+            shared = self.shared_y(int(it[0, 2]), it[:, 1])
         return te_chunks_device(pts, rows0, ns, self.sy.dim, self.sx.dim, self.cfg.k,
                                 self.cfg.jitter_amplitude, np.ascontiguousarray(states),
-                                sync=False, tag=tag)
+                                sync=False, tag=tag, shared=shared)
 
 
 _STREAMS: dict = {}

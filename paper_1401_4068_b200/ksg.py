@@ -16,7 +16,7 @@ import torch
 from scipy import special
 
 from . import _native as nat
-from .engine import MAX_K, search_device
+from .engine import MAX_K, search_device, search_te_shared_device
 from .exceptions import DegenerateData, DomainError, KTooLarge, ShapeMismatch
 
 EULER_GAMMA = 0.5772156649015329
@@ -116,7 +116,7 @@ def te_masks(d_y: int, d_x: int):
 
 
 def te_chunks_device(pts64: torch.Tensor, rows0, ns, d_y: int, d_x: int, k: int,
-                     amplitude: float, seeds, sync: bool = True, tag: str = ""):
+                     amplitude: float, seeds, sync: bool = True, tag: str = "", shared=None):
     """jitter -> checks -> search -> reduce for TE-layout chunks already on the device.
 
     sync=True: returns (te [n_chunks] f64 device tensor or None, status numpy
@@ -131,7 +131,10 @@ def te_chunks_device(pts64: torch.Tensor, rows0, ns, d_y: int, d_x: int, k: int,
         st = status.cpu().numpy()
         if (st != 0).any():
             return None, st
-    _, counts, _ = search_device(pts64, rows0, ns, te_masks(d_y, d_x), k, reuse=True, tag=tag)
+    if shared is not None:  # every chunk pools the same target rows: y marginals once per point
+        _, counts, _ = search_te_shared_device(pts64, rows0, ns, d_y, k, shared, tag=tag)
+    else:
+        _, counts, _ = search_device(pts64, rows0, ns, te_masks(d_y, d_x), k, reuse=True, tag=tag)
     te = te_reduce_device(counts, rows0, ns, k, tag)
     return (te, st) if sync else (te, status)
 
