@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(128) axes_kernel(const ChunkInfo *__restrict__
 // ---------------------------------------------------------------------------
 struct FilterCols {
     int f0, nf, bits;  // columns and Morton bits per column
+    int skip_pca;      // chunks with principal axes need no filter order (kNN-order-only searches)
 };
 
 template <int T>
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(T) sort_kernel(
     const ChunkInfo ci = info[blockIdx.x];
     if (!ci.ok32) return;
     const ColStats *cs = stats + blockIdx.x;
+    if (fc.skip_pca && cs->use_pca) return;
     const uint32_t qmax = (1u << fc.bits) - 1u;
     if (threadIdx.x < fc.nf) {
         const int col = fc.f0 + threadIdx.x;
@@ -1159,6 +1161,7 @@ static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Pl
         }
         FilterCols sfc = p.fc;
         if (!prune) sfc.nf = 0;  // identity order
+        sfc.skip_pca = knn_only ? 1 : 0;
         ENTE_LAUNCH("sort", st,
                     (p.max_npad <= kSortSmallN ? sort_kernel<kSortThreadsSmall> : sort_kernel<kSortThreads>)
                     <<<n_chunks, p.max_npad <= kSortSmallN ? kSortThreadsSmall : kSortThreads, 0, st>>>(pts64, dim, w.info, w.stats, sfc,

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
     uint32_t *qsm = reinterpret_cast<uint32_t *>(x2 + C);  // k-th neighbour records (C)
     int32_t *tab = reinterpret_cast<int32_t *>(qsm + C);   // kSyBins
     int32_t *list = tab + kSyBins;  // queued subtiles (nsub)
-    __shared__ int nlist, nq;
+    __shared__ int nlist, wq_n[kSyThreads / 32];
     __shared__ uint32_t qk[kSyQueue];  // exact checks: k | which << 31
     __shared__ int32_t qq[kSyQueue];   // ... and the neighbour q
     __shared__ int wsum[kSyThreads / 32][2];
@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
         xA[k] = x2[k] = 0;
     }
     for (int k = tid; k <= C; k += kSyThreads) dA[k] = d2[k] = 0;
-    if (tid == 0) nlist = nq = 0;
+    if (tid == 0) nlist = 0;
+    if (tid < kSyThreads / 32) wq_n[tid] = 0;
     double yp[kSyMaxY];
     for (int c = 0; c < g.dd; ++c) yp[c] = y0[(int64_t)p * g.dd + c];
     __syncthreads();
@@ -269,31 +270,31 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
         const int rr = pi < 0 ? point_r : inv_perms[(int64_t)pi * g.reps + point_r];
         return info[c].row0 + (int64_t)rr * g.w + point_t;
     };
-    // the queued exact checks, all threads at once (independent scattered reads
-    // of the jittered rows in flight together instead of one lane's loop)
-    auto drain = [&]() {
-        __syncthreads();
-        const int n = nq < kSyQueue ? nq : kSyQueue;
-        for (int e = tid; e < n; e += kSyThreads) {
-            const uint32_t kw = qk[e];
-            const int k = (int)(kw & 0x7FFFFFFFu), which = (int)(kw >> 31);
-            const int q = qq[e], qr = q / g.w, qt = q - qr * g.w;
-            const int c = cid[k];
-            const int64_t ip = row_in(c, pr, pt);
-            const double *rp = pts64 + ip * dim;
-            const double *rq = pts64 + row_in(c, qr, qt) * dim;
-            double dd = 0.0;
-            for (int col = which ? 0 : 1; col < g.dd; ++col) dd = fmax(dd, fabs(__dsub_rn(rp[col], rq[col])));
-            if (dd < eps[ip]) atomicAdd(which ? &x2[k] : &xA[k], 1);
-        }
-        __syncthreads();
-        if (tid == 0) nq = 0;
-        __syncthreads();
+    // Exact checks are queued per warp and settled by the whole warp at once
+    // (independent scattered reads of the jittered rows in flight together
+    // instead of one lane's loop); no CTA barrier inside the walk.
+    constexpr int QW = kSyQueue / (kSyThreads / 32);
+    uint32_t *wqk = qk + warp * QW;
+    int32_t *wqq = qq + warp * QW;
+    auto check = [&](int k, int which, int q) {
+        const int c = cid[k];
+        const int64_t ip = row_in(c, pr, pt);
+        const double *rp = pts64 + ip * dim;
+        const double *rq = pts64 + row_in(c, q / g.w, q - (q / g.w) * g.w) * dim;
+        double dd = 0.0;
+        for (int col = which ? 0 : 1; col < g.dd; ++col) dd = fmax(dd, fabs(__dsub_rn(rp[col], rq[col])));
+        if (dd < eps[ip]) atomicAdd(which ? &x2[k] : &xA[k], 1);
     };
-    const int steps = (nl + kSyThreads / 32 - 1) / (kSyThreads / 32);
-    for (int it = 0; it < steps; ++it) {  // CTA-uniform trip count: drain() synchronises
-        const int e = it * (kSyThreads / 32) + warp;
-        const int sq = e < nl ? list[e] * 32 + lane : g.m;
+    auto drain = [&]() {  // warp-uniform
+        __syncwarp();
+        const int n = wq_n[warp] < QW ? wq_n[warp] : QW;
+        for (int e = lane; e < n; e += 32) check((int)(wqk[e] & 0x7FFFFFFFu), (int)(wqk[e] >> 31), wqq[e]);
+        __syncwarp();
+        if (lane == 0) wq_n[warp] = 0;
+        __syncwarp();
+    };
+    for (int e = warp; e < nl; e += kSyThreads / 32) {
+        const int sq = list[e] * 32 + lane;
         const int q = sq < g.m ? yperm[sq] : p;
         if (q != p) {
             const double *yq = ys + (int64_t)sq * g.dd;
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
                 if (d0 - g.margin > rmax) continue;  // outside every query
                 const int u = sy_upper(key, tab, C, r0, inv_bw, d0 + g.margin);
                 if (u < C) atomicAdd(which ? &d2[u] : &dA[u], 1);
-                // near the radius (r' >= (d0 - M)(1 - 2^-19)): exact, later
+                // near the radius (r' >= (d0 - M)(1 - 2^-19)): exact, queued
                 const double lo_x = (d0 - g.margin) * (1.0 - 0x1p-19);
                 for (int k = u - 1; k >= 0 && sy_radius(key[k]) >= lo_x; --k) {
                     const uint32_t ks = qsm[k];
@@ -314,29 +315,21 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
                         if ((ks >> (30 + which)) & 1u) atomicAdd(which ? &x2[k] : &xA[k], 1);
                         continue;
                     }
-                    const int slot = atomicAdd(&nq, 1);
-                    if (slot < kSyQueue) {
-                        qk[slot] = (uint32_t)k | ((uint32_t)which << 31);
-                        qq[slot] = q;
-                    } else {  // queue full: settle this one in place
-                        const int c = cid[k];
-                        const int64_t ip = row_in(c, pr, pt);
-                        const double *rp = pts64 + ip * dim;
-                        const double *rq = pts64 + row_in(c, q / g.w, q - (q / g.w) * g.w) * dim;
-                        double dd = 0.0;
-                        for (int col = which ? 0 : 1; col < g.dd; ++col)
-                            dd = fmax(dd, fabs(__dsub_rn(rp[col], rq[col])));
-                        if (dd < eps[ip]) atomicAdd(which ? &x2[k] : &xA[k], 1);
+                    const int slot = atomicAdd(&wq_n[warp], 1);
+                    if (slot < QW) {
+                        wqk[slot] = (uint32_t)k | ((uint32_t)which << 31);
+                        wqq[slot] = q;
+                    } else {
+                        check(k, which, q);  // queue full: settle it in place
                     }
                 }
             }
         }
-        __syncthreads();  // every add of this step is in nq
-        const int pending = nq;
-        __syncthreads();  // (nobody changes nq before every thread has read it)
-        if (pending >= kSyQueue / 2 || it == steps - 1) drain();
+        __syncwarp();
+        if (wq_n[warp] >= QW / 2) drain();
     }
-    if (steps == 0) __syncthreads();
+    drain();
+    __syncthreads();
     // inclusive prefix sums of the difference arrays, chunk by chunk of the CTA
     int runA = 0, run2 = 0;
     for (int base = 0; base < C; base += kSyThreads) {

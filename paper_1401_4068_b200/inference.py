@@ -168,6 +168,7 @@ class PairPipeline:
         self.inv_perm_dev = None
         self.perm_count = 0
         self.target_values = np.asarray(target.values, dtype=np.float64)
+        self.source_values = np.asarray(source.values, dtype=np.float64)
         self._shared = {}
 
     def set_perms(self, perms):
@@ -177,7 +178,28 @@ class PairPipeline:
         np.put_along_axis(inv, arr.astype(np.int64), np.arange(self.reps, dtype=np.int32)[None, :], 1)
         self.inv_perm_dev = torch.from_numpy(np.ascontiguousarray(inv)).to(nat.device())
         self.perm_count = len(perms)
-        self._shared.clear()
+
+    def shared_pays(self, t_lo: int, u: int) -> bool:
+        """Whether the shared-y search is the faster one for this window: its m3
+        / joint sweeps walk the principal-axis order, which only embedded
+        low-dimensional dynamics get (the same test the device applies per
+        chunk: variance off the two leading principal axes < 5 % of the
+        first, >= 4096 points).  Noise-driven data keeps the fused sweep."""
+        key = ("pays", t_lo)
+        hit = self._shared.get(key)
+        if hit is None:
+            hit = False
+            if self.m >= 4096:
+                yv, xv = self.target_values, self.source_values
+                times = np.arange(t_lo, t_lo + self.w)
+                cols = [yv[:, times - 1]] + [yv[:, times - 2 - j * self.sy.delay]
+                                             for j in range(self.sy.dim)]
+                cols += [xv[:, times - 1 - u - j * self.sx.delay] for j in range(self.sx.dim)]
+                joint = np.stack([c.reshape(-1) for c in cols], axis=1)[:, :8]
+                lam = np.sort(np.linalg.eigvalsh(np.cov(joint, rowvar=False)))[::-1]
+                hit = bool(lam[0] > 0 and lam[2:].sum() < 0.05 * lam[0])
+            self._shared[key] = hit
+        return hit
 
     def shared_y(self, t_lo: int, perm_index):
         """SharedY of the window starting at t_lo (every chunk of the window
@@ -283,8 +305,8 @@ class PairPipeline:
         rows0 = np.arange(n, dtype=np.int64) * self.m
         ns = np.full(n, self.m, dtype=np.int64)
         shared = None
-        if SHARED_Y and (it[:, 2] == it[0, 2]).all():  # one window: one target point set
-            shared = self.shared_y(int(it[0, 2]), it[:, 1])
+        if SHARED_Y and (it[:, 2] == it[0, 2]).all() and self.shared_pays(int(it[0, 2]), int(it[0, 0])):
+            shared = self.shared_y(int(it[0, 2]), it[:, 1])  # one window: one target point set
         return te_chunks_device(pts, rows0, ns, self.sy.dim, self.sx.dim, self.cfg.k,
                                 self.cfg.jitter_amplitude, np.ascontiguousarray(states),
                                 sync=False, tag=tag, shared=shared)

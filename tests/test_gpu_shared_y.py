@@ -65,7 +65,7 @@ def test_shared_y_counts_equal_per_chunk_search(kind, amp):
     assert torch.equal(cnt_a, cnt_b)
 
 
-@pytest.mark.parametrize("name", ["C1", "C2"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C5"])
 def test_pipeline_te_unchanged_by_shared_y(name, monkeypatch):
     from paper_1401_4068_b200 import inference
     wl = workloads.CONFIGS[name]
@@ -78,7 +78,23 @@ def test_pipeline_te_unchanged_by_shared_y(name, monkeypatch):
     pipe.set_perms(surrogate_perms(0, s, x.shape[0], True))
     items = [(u, -1) for u in cfg.u_candidates] + [(u, i) for u in cfg.u_candidates for i in range(s)]
     monkeypatch.setattr(inference, "SHARED_Y", True)
+    monkeypatch.setattr(PairPipeline, "shared_pays", lambda self, t, u: True)  # AR data too
     te_shared = pipe.run(items)
     monkeypatch.setattr(inference, "SHARED_Y", False)
     te_sweep = pipe.run(items)
     assert np.array_equal(te_shared, te_sweep)
+
+
+def test_shared_y_is_chosen_for_embedded_dynamics_only():
+    wl = workloads.CONFIGS["C2"]
+    x, y = wl.ensembles()
+    spec = EmbeddingSpec(*wl.spec)
+    cfg = AnalysisConfig(u_candidates=(1,), window=wl.window, k=4, n_surrogates=2, seed=0)
+    assert PairPipeline(EnsembleSeries("X", x), EnsembleSeries("Y", y), spec, spec,
+                        cfg).shared_pays(wl.window[0], 1)
+    wl = workloads.CONFIGS["C5"]
+    x, y = wl.ensembles()
+    spec = EmbeddingSpec(*wl.spec)
+    cfg = AnalysisConfig(u_candidates=(5,), window=wl.window, k=4, n_surrogates=2, seed=0)
+    assert not PairPipeline(EnsembleSeries("X", x), EnsembleSeries("Y", y), spec, spec,
+                            cfg).shared_pays(wl.window[0], 5)
