@@ -1643,8 +1643,8 @@ struct SyBufs {
 };
 
 static size_t sy_smem_bytes(int C, int nsub) {
-    return (size_t)C * 4 * 3 + 2 * (size_t)(C + 1) * 4 + 2 * (size_t)C * 4 + (size_t)kSyBins * 4 +
-           (size_t)nsub * 4;
+    return (size_t)C * 4 * 3 + 2 * (size_t)(C + 1) * 4 + 2 * (size_t)C * 4 + (size_t)nsub * 4 +
+           (size_t)kSyBins * 2;
 }
 
 static SyBufs sy_layout(Arena &a, int64_t m, int C, int dd) {
@@ -1672,7 +1672,7 @@ static bool sy_usable(const Plan &p, int n_chunks, int64_t m, int k) {
     SweepSet ss;
     return p.fast && p.lay.nout == 3 && p.lay.slot[0] == 0 && p.lay.slot[1] == 1 && p.lay.slot[2] == 2 &&
            p.max_npad >= kCompactMinRows && k + 1 <= 16 && find_sweep_set(p.dy, p.dx, ss) &&
-           ss.count3 != nullptr && 1 + p.dy <= kSyMaxY &&
+           ss.count3 != nullptr && 1 + p.dy <= kSyMaxY && n_chunks < 65535 &&
            sy_smem_bytes(n_chunks, (int)((m + 31) / 32)) <= 200 * 1024;
 }
 

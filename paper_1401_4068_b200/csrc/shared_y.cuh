@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) sy_gather_kernel(const double *__restrict
     }
 }
 
-constexpr int kSyBins = 2048;  // lookup table over each point's radius range
+constexpr int kSyBins = 4096;  // lookup table over each point's radius range (uint16 entries)
 
 __device__ __forceinline__ double sy_radius(uint32_t key) {  // truncated radius r' of a key
     return __longlong_as_double((long long)((uint64_t)key << 32));
@@ -181,7 +181,7 @@ __device__ __forceinline__ double sy_radius(uint32_t key) {  // truncated radius
 // first k with r'[k] > x: the lookup table gives a start within a bin of the
 // answer, a short scan finishes it (correct for any table entry: the array is
 // sorted)
-__device__ __forceinline__ int sy_upper(const uint32_t *key, const int32_t *tab, int C, double r0,
+__device__ __forceinline__ int sy_upper(const uint32_t *key, const uint16_t *tab, int C, double r0,
                                         double inv_bw, double x) {
     if (!(x >= r0)) return 0;
     const double fb = (x - r0) * inv_bw;
@@ -216,8 +216,8 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
     int32_t *xA = d2 + C + 1;    // C exact additions
     int32_t *x2 = xA + C;
     uint32_t *qsm = reinterpret_cast<uint32_t *>(x2 + C);  // k-th neighbour records (C)
-    int32_t *tab = reinterpret_cast<int32_t *>(qsm + C);   // kSyBins
-    int32_t *list = tab + kSyBins;  // queued subtiles (nsub)
+    int32_t *list = reinterpret_cast<int32_t *>(qsm + C);  // queued subtiles (nsub)
+    uint16_t *tab = reinterpret_cast<uint16_t *>(list + g.nsub);  // kSyBins
     __shared__ int nlist, wq_n[kSyThreads / 32];
     __shared__ uint32_t qk[kSyQueue];  // exact checks: k | which << 31
     __shared__ int32_t qq[kSyQueue];   // ... and the neighbour q
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
             if (sy_radius(key[mid]) >= edge) hi = mid;
             else lo = mid + 1;
         }
-        tab[b] = lo;
+        tab[b] = (uint16_t)lo;
     }
     const double R = rmax + g.margin;
     const int ny = g.dd - 1;
