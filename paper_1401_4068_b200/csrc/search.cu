@@ -350,6 +350,9 @@ __device__ __forceinline__ uint32_t spread15(uint32_t v) {  // bits 0..14 -> eve
     return v;
 }
 
+#ifndef ENTE_PCA_BITS
+#define ENTE_PCA_BITS 8  // Morton bits per principal axis of the kNN order (12: same pruning, 3 radix passes)
+#endif
 template <int T>
 __global__ void __launch_bounds__(T) sort_pca_kernel(
     const double *__restrict__ pts64, int dim, const ChunkInfo *__restrict__ info,
@@ -413,7 +416,7 @@ __global__ void __launch_bounds__(T) sort_pca_kernel(
         mn1 = fminf(mn1, red[2][w]);
         mx1 = fmaxf(mx1, red[3][w]);
     }
-    const float q = 4095.0f;  // 12 bits per axis: 24-bit keys, three radix passes
+    const float q = (float)((1 << ENTE_PCA_BITS) - 1);  // bits per axis (radix passes = 2 bits / 8)
     const float s0 = mx0 > mn0 ? q / (mx0 - mn0) : 0.0f;
     const float s1 = mx1 > mn1 ? q / (mx1 - mn1) : 0.0f;
     for (int i = threadIdx.x; i < ci.n; i += T) {  // same thread, same i: no barrier needed
@@ -424,7 +427,7 @@ __global__ void __launch_bounds__(T) sort_pca_kernel(
         v0[i] = i;
     }
     __syncthreads();
-    const int par = cta_radix_sort<T, uint32_t, int32_t>(k0, k1, v0, v1, ci.n, 24, sm);
+    const int par = cta_radix_sort<T, uint32_t, int32_t>(k0, k1, v0, v1, ci.n, 2 * ENTE_PCA_BITS, sm);
     const int32_t *res = par ? v1 : v0;
     for (int i = threadIdx.x; i < ci.n; i += T) perm[ci.row0 + i] = res[i];
 }
