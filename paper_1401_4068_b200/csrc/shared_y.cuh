@@ -243,15 +243,21 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
     const double rmax = sy_radius(key[C - 1]) * (1.0 + 0x1p-19);  // >= every exact radius
     const double bw = (rmax - r0) / kSyBins;
     const double inv_bw = bw > 0.0 ? 1.0 / bw : 0.0;
-    for (int b = tid; b < kSyBins; b += kSyThreads) {  // tab[b] = first k with r'_k >= r0 + b bw
-        const double edge = r0 + b * bw;
+    {  // tab[b] = first k with r'_k >= r0 + b bw: one search per thread, then a merge
+        constexpr int PER = kSyBins / kSyThreads;
+        const int b0 = tid * PER;
+        double edge = r0 + b0 * bw;
         int lo = 0, hi = C;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             if (sy_radius(key[mid]) >= edge) hi = mid;
             else lo = mid + 1;
         }
-        tab[b] = (uint16_t)lo;
+        for (int b = b0; b < b0 + PER; ++b) {
+            edge = r0 + b * bw;
+            while (lo < C && sy_radius(key[lo]) < edge) ++lo;
+            tab[b] = (uint16_t)lo;
+        }
     }
     const double R = rmax + g.margin;
     const int ny = g.dd - 1;
@@ -330,11 +336,33 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
     }
     drain();
     __syncthreads();
-    // inclusive prefix sums of the difference arrays, chunk by chunk of the CTA
+    // inclusive prefix sums of the difference arrays: every warp scans its
+    // contiguous share of the C queries after one exchange of warp totals
+    constexpr int NW = kSyThreads / 32;
+    const int per = (C + NW - 1) / NW, k0 = warp * per, k1 = min(C, k0 + per);
+    int sA = 0, s2 = 0;
+    for (int k = k0 + lane; k < k1; k += 32) {
+        sA += dA[k];
+        s2 += d2[k];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sA += __shfl_xor_sync(0xffffffffu, sA, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+        wsum[warp][0] = sA;
+        wsum[warp][1] = s2;
+    }
+    __syncthreads();
     int runA = 0, run2 = 0;
-    for (int base = 0; base < C; base += kSyThreads) {
-        const int k = base + tid;
-        int vA = k < C ? dA[k] : 0, v2 = k < C ? d2[k] : 0;
+    for (int w2 = 0; w2 < warp; ++w2) {
+        runA += wsum[w2][0];
+        run2 += wsum[w2][1];
+    }
+    for (int base = k0; base < k1; base += 32) {
+        const int k = base + lane;
+        int vA = k < k1 ? dA[k] : 0, v2 = k < k1 ? d2[k] : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int tA = __shfl_up_sync(0xffffffffu, vA, o), t2 = __shfl_up_sync(0xffffffffu, v2, o);
@@ -343,30 +371,14 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
                 v2 += t2;
             }
         }
-        if (lane == 31) {
-            wsum[warp][0] = vA;
-            wsum[warp][1] = v2;
-        }
-        __syncthreads();
-        int pA = runA, p2 = run2;
-        for (int w2 = 0; w2 < warp; ++w2) {
-            pA += wsum[w2][0];
-            p2 += wsum[w2][1];
-        }
-        int totA = runA, tot2 = run2;
-        for (int w2 = 0; w2 < kSyThreads / 32; ++w2) {
-            totA += wsum[w2][0];
-            tot2 += wsum[w2][1];
-        }
-        if (k < C) {
+        if (k < k1) {
             const int c = cid[k];
             const int64_t row = row_in(c, pr, pt);
-            out_counts[row] = pA + vA + xA[k];
-            out_counts[total_rows + row] = p2 + v2 + x2[k];
+            out_counts[row] = runA + vA + xA[k];
+            out_counts[total_rows + row] = run2 + v2 + x2[k];
         }
-        runA = totA;
-        run2 = tot2;
-        __syncthreads();
+        runA += __shfl_sync(0xffffffffu, vA, 31);
+        run2 += __shfl_sync(0xffffffffu, v2, 31);
     }
 }
 
