@@ -31,7 +31,10 @@
 
 namespace ente {
 
-constexpr int kSyThreads = 256;
+#ifndef ENTE_SY_THREADS
+#define ENTE_SY_THREADS 256
+#endif
+constexpr int kSyThreads = ENTE_SY_THREADS;
 constexpr int kSyQueue = 1024;  // pending exact checks per CTA (shared memory)
 constexpr int kSyMaxY = 9;  // y columns (1 + d_y), d_y <= 8
 
