@@ -1639,7 +1639,7 @@ extern "C" int ente_search_split(const double *pts64, int64_t total_rows, int di
 // original point for the whole batch.
 // ---------------------------------------------------------------------------
 struct SyBufs {
-    int32_t *chunk_perm, *va, *vb, *parity, *yva, *yvb, *yperm;
+    int32_t *chunk_perm, *va, *vb, *parity, *yva, *yvb, *yperm, *tile3;
     uint32_t *ka, *kb, *kstar, *qs;
     uint32_t *yka, *ykb;
     double *ys, *box;
@@ -1654,6 +1654,7 @@ static SyBufs sy_layout(Arena &a, int64_t m, int C, int dd) {
     SyBufs b{};
     const int nsub = (int)((m + 31) / 32);
     b.chunk_perm = a.take<int32_t>(C);
+    b.tile3 = a.take<int32_t>(2 * C + 1);
     b.ka = a.take<uint32_t>((size_t)m * C);
     b.kb = a.take<uint32_t>((size_t)m * C);
     b.va = a.take<int32_t>((size_t)m * C);
@@ -1755,6 +1756,17 @@ extern "C" int ente_search_te_shared(const double *pts64, int64_t total_rows, in
                               cudaMemcpyHostToDevice, st));
     SweepSet ss;
     find_sweep_set(p.dy, p.dx, ss);
+    // the m3 / joint sweep takes groups of 32 * ENTE_KO_RT references
+    constexpr int kWr3 = 32 * count_rt<true>();
+    std::vector<int32_t> htile3(2 * n_chunks + 1, 0);
+    int32_t ntiles3 = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+        htile3[c] = ntiles3;
+        if (k <= chunks[c].n - 1) ntiles3 += (chunks[c].n + kWr3 - 1) / kWr3;
+    }
+    htile3[n_chunks] = ntiles3;
+    ENTE_CUDA(cudaMemcpyAsync(b.tile3, htile3.data(), sizeof(int32_t) * (2 * n_chunks + 1),
+                              cudaMemcpyHostToDevice, st));
     if (ntiles > 0) {
         const unsigned nt = (unsigned)ntiles;
         const KnnFn knn_fn = knn_table(p.dy, p.dx, p.slots, p.max_npad);
@@ -1765,7 +1777,8 @@ extern "C" int ente_search_te_shared(const double *pts64, int64_t total_rows, in
                                               nullptr, w_.t32, w_.L, work));
         ENTE_CUDA(cudaGetLastError());
         ENTE_LAUNCH("count_pass", st,
-                    ss.count3<<<nt, 32, 0, st>>>(w_.pts32k, w_.fboxk, w_.info, w_.tile0, n_chunks, w_.t32,
+                    ss.count3<<<(unsigned)ntiles3, 32, 0, st>>>(w_.pts32k, w_.fboxk, w_.info, b.tile3,
+                                                               n_chunks, w_.t32,
                                                  ws_rows, prune, w_.cnt3, w_.ev, w_.ev_n, 4u | 8u,
                                                  work + 1));
         ENTE_CUDA(cudaGetLastError());
