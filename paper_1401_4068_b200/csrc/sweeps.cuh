@@ -48,7 +48,7 @@ constexpr int kGate = 4;                    // gate columns in the Morton key an
 #define ENTE_KNNC_UNROLL 1   // compacted kNN pass: row-pair iterations per loop trip
 #endif
 #ifndef ENTE_KO_RT
-#define ENTE_KO_RT 4  // references per lane of the shared-y m3/joint sweep
+#define ENTE_KO_RT 3  // references per lane of the shared-y m3/joint sweep (96-reference groups)
 #endif
 #ifndef ENTE_CNT_MINB
 #define ENTE_CNT_MINB 32
@@ -948,7 +948,7 @@ struct CountRefs {
 
 // references per lane of the count sweeps: the KO sweep visits few rows per
 // (reference, sub-tile) in the principal-axis order, so 128-reference groups
-// amortise the walk better (C2: 36.1 -> 31.7 ms measured with 128 everywhere)
+// amortise the walk better (C2 count sweep, ms: 64 refs 34.5, 96 31.8, 128 32.3, 256 44.3)
 template <bool KO>
 __host__ __device__ constexpr int count_rt() { return KO ? ENTE_KO_RT : kRT; }
 
