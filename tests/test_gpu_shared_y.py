@@ -98,3 +98,30 @@ def test_shared_y_is_chosen_for_embedded_dynamics_only():
     cfg = AnalysisConfig(u_candidates=(5,), window=wl.window, k=4, n_surrogates=2, seed=0)
     assert not PairPipeline(EnsembleSeries("X", x), EnsembleSeries("Y", y), spec, spec,
                             cfg).shared_pays(wl.window[0], 5)
+
+
+@pytest.mark.parametrize("dy,dx,k", [(1, 4, 4), (4, 2, 7), (3, 3, 20)])
+def test_shared_y_other_layouts_and_k(dy, dx, k):
+    """d_y = 1 and 4, k = 7, and k = 20 (beyond the shared-y sweep's register
+    lists: the call falls back to the general search) -- always the same counts."""
+    x, y = workloads.lorenz_pair(5, 50, 200, gamma_schedule=lambda t: 0.3, seed=3)
+    spec_x, spec_y = EmbeddingSpec(dx, 1), EmbeddingSpec(dy, 1)
+    cfg = AnalysisConfig(u_candidates=(3,), window=(121, 200), k=k, n_surrogates=12, seed=4)
+    pipe = PairPipeline(EnsembleSeries("X", x), EnsembleSeries("Y", y), spec_x, spec_y, cfg)
+    pipe.set_perms(surrogate_perms(4, 12, x.shape[0], True))
+    items = pipe._items([(3, -1)] + [(3, i) for i in range(12)])
+    from paper_1401_4068_b200 import _native as nat
+    n = len(items)
+    pts = torch.empty((n * pipe.m, pipe.dim), dtype=torch.float64, device="cuda")
+    nat.check(nat.lib().ente_pack_te_items(
+        nat.ptr(pipe.x), nat.ptr(pipe.y), pipe.reps, pipe.n_samples, dx, 1, dy, 1, pipe.w,
+        items.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_int32)), n, nat.ptr(pipe.perm_dev),
+        nat.ptr(pts), nat.stream_handle()), "pack")
+    rows0 = np.arange(n, dtype=np.int64) * pipe.m
+    ns = np.full(n, pipe.m, dtype=np.int64)
+    jitter_device(pts, rows0, ns, 1e-8, pipe._states(items))
+    eps_a, cnt_a, _ = search_device(pts, rows0, ns, te_masks(dy, dx), k)
+    eps_a, cnt_a = eps_a.clone(), cnt_a.clone()
+    eps_b, cnt_b, st = search_te_shared_device(pts, rows0, ns, dy, k, pipe.shared_y(121, items[:, 1]))
+    assert not st.cpu().numpy().any()
+    assert torch.equal(eps_a, eps_b) and torch.equal(cnt_a, cnt_b)
