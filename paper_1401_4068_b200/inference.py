@@ -182,20 +182,21 @@ class PairPipeline:
     def shared_pays(self, t_lo: int, u: int) -> bool:
         """Whether the shared-y search is the faster one for this window: its m3
         / joint sweeps walk the principal-axis order, which only embedded
-        low-dimensional dynamics get (the same test the device applies per
-        chunk: variance off the two leading principal axes < 5 % of the
-        first, >= 4096 points).  Noise-driven data keeps the fused sweep."""
+        low-dimensional dynamics get (the test the device applies per chunk:
+        variance off the two leading principal axes < 5 % of the first,
+        >= 4096 points; here on every 4th repetition of the window's first
+        chunk).  Noise-driven data keeps the fused sweep."""
         key = ("pays", t_lo)
         hit = self._shared.get(key)
         if hit is None:
             hit = False
             if self.m >= 4096:
-                yv, xv = self.target_values, self.source_values
+                yv, xv = self.target_values[::4], self.source_values[::4]
                 times = np.arange(t_lo, t_lo + self.w)
                 cols = [yv[:, times - 1]] + [yv[:, times - 2 - j * self.sy.delay]
                                              for j in range(self.sy.dim)]
                 cols += [xv[:, times - 1 - u - j * self.sx.delay] for j in range(self.sx.dim)]
-                joint = np.stack([c.reshape(-1) for c in cols], axis=1)[:, :8]
+                joint = np.stack([c.reshape(-1) for c in cols[:8]], axis=1)
                 lam = np.sort(np.linalg.eigvalsh(np.cov(joint, rowvar=False)))[::-1]
                 hit = bool(lam[0] > 0 and lam[2:].sum() < 0.05 * lam[0])
             self._shared[key] = hit
@@ -204,17 +205,20 @@ class PairPipeline:
     def shared_y(self, t_lo: int, perm_index):
         """SharedY of the window starting at t_lo (every chunk of the window
         pools the same target rows): the unjittered y columns
-        (embedding.py:109-113) and the jitter margin 2 hw + rounding, hw =
-        amplitude x the columns' std (ksg.py:52-59)."""
+        (embedding.py:109-113), gathered on the device from the resident
+        target, and the jitter margin 2 hw + rounding, hw = amplitude x the
+        columns' std (ksg.py:52-59)."""
         hit = self._shared.get(t_lo)
         if hit is None:
             yv = self.target_values
             times = np.arange(t_lo, t_lo + self.w)
-            cols = [yv[:, times - 1]] + [yv[:, times - 2 - j * self.sy.delay] for j in range(self.sy.dim)]
-            y0 = np.ascontiguousarray(np.stack([c.reshape(-1) for c in cols], axis=1))
-            hw = self.cfg.jitter_amplitude * float(y0.std(axis=0).max()) * (1.0 + 1e-9)
-            margin = 2.0 * hw * (1.0 + 1e-12) + 2.0 ** -48 * (float(np.abs(y0).max()) + hw)
-            hit = (torch.from_numpy(y0).to(nat.device()), margin)
+            idx = [times - 1] + [times - 2 - j * self.sy.delay for j in range(self.sy.dim)]
+            hw = self.cfg.jitter_amplitude * max(float(yv[:, ix].std()) for ix in idx) * (1.0 + 1e-9)
+            vmax = max(float(np.abs(yv[:, ix]).max()) for ix in idx)
+            margin = 2.0 * hw * (1.0 + 1e-12) + 2.0 ** -48 * (vmax + hw)
+            cols = torch.from_numpy(np.stack(idx, axis=1).reshape(-1)).to(self.y.device)
+            y0 = self.y[:, cols].reshape(self.reps, self.w, len(idx)).reshape(self.m, len(idx))
+            hit = (y0.contiguous(), margin)
             self._shared[t_lo] = hit
         y0, margin = hit
         if self.perm_dev is None:
