@@ -14,12 +14,15 @@ import os
 import shutil
 import subprocess
 import sys
+import sysconfig
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "ente_b200")
 LIB = os.path.join(PKG, "libente_b200.so")
+PYHOST_SRC = os.path.join(CSRC, "pyhost.cpp")
+PYHOST = os.path.join(PKG, "_pyhost" + sysconfig.get_config_var("EXT_SUFFIX"))
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -49,9 +52,26 @@ def _needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def build_pyhost(force: bool = False) -> str:
+    """The CPython host helper (_pyhost: chunk pointers via the buffer protocol)."""
+    if not force and os.path.exists(PYHOST) and os.path.getmtime(PYHOST) > os.path.getmtime(PYHOST_SRC):
+        return PYHOST
+    cxx = shutil.which("g++") or "c++"
+    tmp = PYHOST + ".tmp"
+    cmd = [cxx, "-O2", "-shared", "-fPIC", "-std=c++17", "-I", sysconfig.get_paths()["include"],
+           PYHOST_SRC, "-o", tmp]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"g++ failed for {PYHOST_SRC}:\n{r.stderr}")
+    os.replace(tmp, PYHOST)
+    return PYHOST
+
+
 def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
     """Compile and link; `defines` (-D flags) + `out` make development variants."""
     lib_path = out or LIB
+    if out is None and not defines:
+        build_pyhost(force)
     if not force and not defines and out is None and not _needs_build():
         return LIB
     bdir = BUILD if not defines else BUILD + "_" + "_".join(d.replace("=", "") for d in defines)

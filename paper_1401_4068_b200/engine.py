@@ -15,6 +15,7 @@ bit-identical to the reference's fp64 sweep.
 from __future__ import annotations
 
 import ctypes
+import gc
 import os
 import threading
 import warnings
@@ -182,69 +183,171 @@ def search_te_shared_device(pts64: torch.Tensor, rows0, ns, d_y: int, k: int, sh
 
 
 class _Pinned(threading.local):
-    buf = None
+    bufs = None
 
 
 _pinned = _Pinned()
 
 
-def _pinned_buffer(nbytes: int) -> torch.Tensor:
+def _pinned_buffer(nbytes: int, slot: int = 0) -> torch.Tensor:
     """Grow-only pinned host staging buffer (page-locking per call costs more than the copy)."""
-    buf = _pinned.buf
+    if _pinned.bufs is None:
+        _pinned.bufs = {}
+    buf = _pinned.bufs.get(slot)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8).pin_memory()
-        _pinned.buf = buf
+        _pinned.bufs[slot] = buf
     return buf
 
 
-def _upload(points_list):
+try:  # chunk pointers through the buffer protocol in C (csrc/pyhost.cpp)
+    from . import _pyhost
+except ImportError:  # not built: the same values one Python attribute at a time
+    _pyhost = None
+
+
+def _scan(points_list):
+    """(addresses, byte sizes, rows) of C-contiguous arrays as int64 numpy arrays."""
+    if _pyhost is not None:
+        a, b, r = _pyhost.scan(points_list)
+        return (np.frombuffer(a, dtype=np.int64), np.frombuffer(b, dtype=np.int64),
+                np.frombuffer(r, dtype=np.int64))
+    n = len(points_list)
+    return (np.fromiter((p.ctypes.data for p in points_list), dtype=np.int64, count=n),
+            np.fromiter((p.nbytes for p in points_list), dtype=np.int64, count=n),
+            np.fromiter((p.shape[0] for p in points_list), dtype=np.int64, count=n))
+
+
+def _upload(points_list, slot: int = 0, tag: str = "", scan=None):
     """Concatenate the chunks straight into pinned memory (multi-threaded,
-    ente_host_gather) and copy them to the device in one transfer."""
-    rows = sum(p.shape[0] for p in points_list)
+    ente_host_gather) and copy them to the device in one transfer on the
+    current stream.  Staging slot `slot` must be free (its previous copy done).
+    scan: _scan(points_list), when the caller has it."""
+    addrs, sizes, ns = scan if scan is not None else _scan(points_list)
+    rows = int(ns.sum())
     dim = points_list[0].shape[1]
-    stage = _pinned_buffer(rows * dim * 8)[:rows * dim * 8].view(torch.float64).view(rows, dim)
-    if len(points_list) == 1:
-        np.copyto(stage.numpy(), points_list[0])
-    else:
-        n = len(points_list)
-        srcs = (ctypes.c_void_p * n)(*[p.ctypes.data for p in points_list])
-        sizes = np.fromiter((p.nbytes for p in points_list), dtype=np.int64, count=n)
-        nat.check(nat.lib().ente_host_gather(srcs, sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-                                             n, stage.data_ptr()), "ente_host_gather")
-    dev = nat.scratch("engine.points", (rows, dim), torch.float64)
+    stage = _pinned_buffer(rows * dim * 8, slot)[:rows * dim * 8].view(torch.float64).view(rows, dim)
+    addrs = np.ascontiguousarray(addrs)
+    sizes = np.ascontiguousarray(sizes)
+    nat.check(nat.lib().ente_host_gather(addrs.ctypes.data_as(ctypes.POINTER(ctypes.c_void_p)),
+                                         sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                         len(addrs), stage.data_ptr()), "ente_host_gather")
+    dev = nat.scratch("engine.points" + tag, (rows, dim), torch.float64)
     dev.copy_(stage, non_blocking=True)
     return dev
 
 
-def _run_group(points_list, dim, masks, k):
+PIPE_BYTES = int(os.environ.get("ENTE_PIPE_MB", "96")) << 20  # host-input bytes per pipelined part of a batch_search wave
+_PIPE_STREAMS: dict = {}
+
+
+def _pipe_streams():
+    key = torch.cuda.current_device()
+    s = _PIPE_STREAMS.get(key)
+    if s is None:
+        s = _PIPE_STREAMS[key] = (torch.cuda.Stream(), torch.cuda.Stream())
+    return s
+
+
+def _parts(ns, dim):
+    """Contiguous chunk ranges of about PIPE_BYTES of input each."""
+    limit = max(1, PIPE_BYTES // (8 * dim))
+    bounds, acc = [0], 0
+    for i, n in enumerate(ns.tolist()):
+        if acc and acc + n > limit:
+            bounds.append(i)
+            acc = 0
+        acc += n
+    bounds.append(len(ns))
+    return list(zip(bounds[:-1], bounds[1:]))
+
+
+def _new_counts(eps, cnts):
+    o = object.__new__(NeighborCounts)  # frozen dataclass: fill the instance dict directly
+    d = o.__dict__
+    d["kth_distance"] = eps
+    d["radius_counts"] = cnts
+    return o
+
+
+def _run_group(points_list, dim, masks, k, scan=None):
+    """One wave: upload, search and read back, pipelined in parts of about
+    PIPE_BYTES on two streams so the host gather and the PCIe copies of one
+    part overlap the searches of the others."""
     search_path(dim, masks, k)
-    ns = np.fromiter((p.shape[0] for p in points_list), dtype=np.int64, count=len(points_list))
-    rows0 = np.concatenate([[0], np.cumsum(ns)[:-1]]).astype(np.int64)
-    dev = _upload(points_list)
-    eps, counts, status = search_device(dev, rows0, ns, masks, k, reuse=True)
+    n_chunks = len(points_list)
+    addrs, sizes, ns = scan if scan is not None else _scan(points_list)
+    rows0 = np.zeros(n_chunks, dtype=np.int64)
+    np.cumsum(ns[:-1], out=rows0[1:])
+    total = int(ns.sum())
+    nm = len(masks)
     # results land in fresh pinned host tensors (torch's caching host allocator:
     # no page-locking or first-touch per call), counts widened to int64 on the
     # device, so the host does no conversion pass
-    nm = len(masks)
-    eps_p = torch.empty(eps.shape, dtype=torch.float64, pin_memory=True)
-    eps_p.copy_(eps, non_blocking=True)
-    cnt_p = torch.empty(counts.shape, dtype=torch.int64, pin_memory=True)
-    if nm:
-        cnt_p.copy_(counts.to(torch.int64), non_blocking=True)
-    st_h = status.cpu().numpy()  # synchronises the stream
-    eps_h, cnt_h = eps_p.numpy(), cnt_p.numpy()
-    rows = [cnt_h[m] for m in range(nm)]
-    out = []
-    for i, (r0, n) in enumerate(zip(rows0.tolist(), ns.tolist())):
-        code = st_h[i]
-        if code == nat.CHUNK_NONFINITE:
-            out.append(ShapeMismatch("chunk contains non-finite values"))
-        elif code == nat.CHUNK_K_TOO_LARGE:
-            out.append(KTooLarge(f"k={k} not in [1, n-1] for n={n}"))
+    eps_p = torch.empty(total, dtype=torch.float64, pin_memory=True)
+    # one 1-D tensor per marginal: each part's slice is contiguous, so its
+    # copy stays a single async DMA (a strided pinned slice would be copied
+    # through a pageable temporary, synchronously)
+    cnt_p = [torch.empty(total, dtype=torch.int64, pin_memory=True) for _ in range(nm)]
+    st_p = torch.empty(n_chunks, dtype=torch.int32, pin_memory=True)
+    parts = _parts(ns, dim)
+    main = torch.cuda.current_stream()
+    streams = _pipe_streams() if len(parts) > 1 else (main,)
+    staged = [None] * len(streams)  # event: the slot's previous H2D is done
+    for j, (a, b) in enumerate(parts):
+        slot = j % len(streams)
+        st = streams[slot]
+        if st is not main:
+            st.wait_stream(main)
+        if staged[slot] is not None:
+            staged[slot].synchronize()
+        r0, r1 = int(rows0[a]), int(rows0[b - 1] + ns[b - 1])
+        tag = f".p{slot}" if len(parts) > 1 else ""
+        with torch.cuda.stream(st):
+            dev = _upload(points_list[a:b], slot, tag, (addrs[a:b], sizes[a:b], ns[a:b]))
+            ev = torch.cuda.Event()
+            ev.record(st)
+            staged[slot] = ev
+            eps, counts, status = search_device(dev, rows0[a:b] - r0, ns[a:b], masks, k, reuse=True,
+                                                tag=tag)
+            eps_p[r0:r1].copy_(eps, non_blocking=True)
+            if nm:
+                c64 = counts.to(torch.int64)
+                for m in range(nm):
+                    cnt_p[m][r0:r1].copy_(c64[m], non_blocking=True)
+            st_p[a:b].copy_(status, non_blocking=True)
+    for st in streams:
+        st.synchronize()
+    st_h, eps_h, cnt_h = st_p.numpy(), eps_p.numpy(), [c.numpy() for c in cnt_p]
+    return _assemble(st_h, eps_h, cnt_h, rows0, ns, k)
+
+
+def _assemble(st_h, eps_h, cnt_h, rows0, ns, k):
+    """Per-chunk NeighborCounts views into one call's result arrays."""
+    n_chunks, nm = len(ns), len(cnt_h)
+    gc_on = gc.isenabled()
+    gc.disable()  # tens of thousands of small containers: no collector passes meanwhile
+    try:
+        if n_chunks > 1 and (ns == ns[0]).all():  # uniform chunks: row views made in C
+            n = int(ns[0])
+            es = list(eps_h.reshape(n_chunks, n))
+            cs = zip(*[list(c.reshape(n_chunks, n)) for c in cnt_h]) if nm else [()] * n_chunks
+            out = [_new_counts(e, c) for e, c in zip(es, cs)]
         else:
-            # views into this call's fresh result arrays (nothing else holds them)
-            end = r0 + n
-            out.append(NeighborCounts(eps_h[r0:end], tuple([r[r0:end] for r in rows])))
+            out = []
+            for r0, n in zip(rows0.tolist(), ns.tolist()):
+                end = r0 + n
+                out.append(_new_counts(eps_h[r0:end], tuple([c[r0:end] for c in cnt_h])))
+        bad = np.flatnonzero(st_h)
+        for i in bad.tolist():
+            code = st_h[i]
+            if code == nat.CHUNK_NONFINITE:
+                out[i] = ShapeMismatch("chunk contains non-finite values")
+            elif code == nat.CHUNK_K_TOO_LARGE:
+                out[i] = KTooLarge(f"k={k} not in [1, n-1] for n={int(ns[i])}")
+    finally:
+        if gc_on:
+            gc.enable()
     return out
 
 
@@ -258,8 +361,8 @@ def batch_search(items: Sequence, k: int):
     results = [None] * len(items)
     fast = _uniform_batch(items, k)
     if fast is not None:  # one validated layout for every chunk: no per-item checks
-        dim, masks, pts_list = fast
-        _run_waves(list(enumerate(pts_list)), dim, masks, k, results)
+        dim, masks, pts_list, scan = fast
+        _run_waves(list(enumerate(pts_list)), dim, masks, k, results, scan)
         return results
     groups = {}
     mask_cache = {}  # (id(marginals), dim) -> (marginals, masks): items usually share one list
@@ -301,32 +404,37 @@ def _uniform_batch(items, k):
     first = items[0][1]
     if any(m is not first for _, m in items) or not all(type(c) is Chunk for c, _ in items):
         return None
-    pts_list = [c.points for c, _ in items]  # Chunk validated these (fp64, contiguous, finite)
-    shapes = np.array([p.shape for p in pts_list], dtype=np.int64)
-    dim = int(shapes[0, 1])
-    if (shapes[:, 1] != dim).any() or k < 1 or k > int(shapes[:, 0].min()) - 1:
-        return None
+    pts_list = [c.points for c, _ in items]  # Chunk validated these (fp64, 2-D, contiguous, finite)
+    scan = _scan(pts_list)
+    dim = int(pts_list[0].shape[1])
+    if (scan[1] != scan[2] * (8 * dim)).any() or k < 1 or k > int(scan[2].min()) - 1:
+        return None  # mixed widths, or k out of range for some chunk
     try:
         masks = tuple(column_mask(cols, dim) for cols in first)
     except ShapeMismatch:
         return None
     if dim > MAX_DIM or k > MAX_K or len(masks) > MAX_MARG:
         return None
-    return dim, masks, pts_list
+    return dim, masks, pts_list, scan
 
 
-def _run_waves(members, dim, masks, k, results):
+def _run_waves(members, dim, masks, k, results, scan=None):
     """Device waves of at most MAX_WAVE_ROWS points (the search workspace is a
-    few hundred bytes per point); members are (slot, points) pairs."""
+    few hundred bytes per point); members are (slot, points) pairs, scan their
+    _scan() when the caller has it."""
+    pts = [p for _, p in members]
+    if scan is None:
+        scan = _scan(pts)
+    ns = scan[2]
     start = 0
     while start < len(members):
         stop, rows = start, 0
-        while stop < len(members) and (stop == start or rows + len(members[stop][1]) <= MAX_WAVE_ROWS):
-            rows += len(members[stop][1])
+        while stop < len(members) and (stop == start or rows + int(ns[stop]) <= MAX_WAVE_ROWS):
+            rows += int(ns[stop])
             stop += 1
-        wave = members[start:stop]
-        outs = _run_group([p for _, p in wave], dim, list(masks), k)
-        for (slot, _), res in zip(wave, outs):
+        outs = _run_group(pts[start:stop], dim, list(masks), k,
+                          tuple(a[start:stop] for a in scan))
+        for (slot, _), res in zip(members[start:stop], outs):
             results[slot] = res
         start = stop
 

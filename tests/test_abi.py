@@ -8,6 +8,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 from paper_1401_4068_b200 import _native as nat
@@ -70,3 +71,19 @@ def test_workspace_sizes_are_host_only():
 
 def test_chunk_struct_layout():
     assert ctypes.sizeof(nat.ChunkDesc) == 16
+
+
+def test_pyhost_scan_matches_numpy_attributes():
+    """The C buffer-protocol scan (csrc/pyhost.cpp) built beside the library
+    reports each chunk's data pointer, byte size and row count."""
+    from paper_1401_4068_b200 import engine
+
+    assert engine._pyhost is not None, "_pyhost was not built (python -m paper_1401_4068_b200.build)"
+    rng = np.random.default_rng(0)
+    arrs = [np.ascontiguousarray(rng.standard_normal((int(n), 5))) for n in rng.integers(1, 50, 30)]
+    a, s, r = engine._scan(arrs)
+    assert a.tolist() == [x.ctypes.data for x in arrs]
+    assert s.tolist() == [x.nbytes for x in arrs]
+    assert r.tolist() == [x.shape[0] for x in arrs]
+    with pytest.raises((BufferError, ValueError)):  # numpy: ValueError, not C-contiguous
+        engine._scan([np.zeros((4, 4))[:, ::2]])

@@ -156,6 +156,38 @@ def test_batch_equals_singles():
         assert all(np.array_equal(x, y) for x, y in zip(s.radius_counts, b.radius_counts))
 
 
+@pytest.mark.parametrize("uniform", [True, False])
+def test_pipelined_parts_equal_one_wave(monkeypatch, uniform):
+    """batch_search waves are uploaded / searched / read back in parts of
+    PIPE_BYTES on two streams; tiny parts must give the one-part results,
+    slot for slot, with the per-slot errors of mixed batches in place."""
+    from paper_1401_4068_b200 import engine
+
+    rng = np.random.default_rng(11)
+    sizes = [700] * 40 if uniform else rng.integers(20, 1500, 40).tolist()
+    chunks = [Chunk(rng.standard_normal((int(n), 7))) for n in sizes]
+    margs = cases.te_margs(3, 3)
+    items = [(c, margs) for c in chunks]
+    if not uniform:  # per-slot errors in the middle of the batch
+        items[5] = (chunks[5], [[0, 9]])
+        items[17] = (Chunk(rng.standard_normal((3, 7))), margs)
+    whole = batch_search(items, 4)
+    monkeypatch.setattr(engine, "PIPE_BYTES", 64 << 10)  # ~ 1 to 3 chunks per part
+    parts = batch_search(items, 4)
+    for a, b in zip(whole, parts):
+        if isinstance(a, Exception):
+            assert type(a) is type(b)
+            continue
+        assert np.array_equal(a.kth_distance, b.kth_distance)
+        assert all(np.array_equal(x, y) for x, y in zip(a.radius_counts, b.radius_counts))
+    for i in (0, 13, 39):
+        eps, cnts = oracle.search(chunks[i].points, margs, 4)
+        assert np.array_equal(parts[i].kth_distance, eps)
+        assert all(np.array_equal(x, y) for x, y in zip(parts[i].radius_counts, cnts))
+    if not uniform:
+        assert isinstance(parts[5], ShapeMismatch) and isinstance(parts[17], KTooLarge)
+
+
 @pytest.mark.parametrize("subset", [(0,), (1,), (2,), (1, 2), (2, 0), ()])
 def test_marginal_subsets_choose_exact_filter(subset):
     # every subset of the TE marginals selects its own pruning columns
