@@ -209,6 +209,10 @@ __device__ __forceinline__ float warp_max_nonneg(float v) {
 // ---------------------------------------------------------------------------
 // A sub-tile box: Q float4 quads of column minima, then Q of maxima
 // (fbox layout per sub-tile: lo[4Q] | hi[4Q], float4 index st * 2Q).
+#ifndef ENTE_GAP_FADD2
+#define ENTE_GAP_FADD2 1
+#endif
+
 template <int Q>
 struct Box {
     float4 lo[Q], hi[Q];
@@ -226,9 +230,18 @@ __device__ __forceinline__ Box<Q> load_box(const float4 *__restrict__ fb, int st
 }
 
 __device__ __forceinline__ float gap4(float4 lo, float4 hi, float4 blo, float4 bhi) {
+#if ENTE_GAP_FADD2
+    // two columns per FADD2 (same roundings as the scalar form)
+    const float2 a = __fadd2_rn(make_float2(lo.x, lo.y), make_float2(-bhi.x, -bhi.y));
+    const float2 b = __fadd2_rn(make_float2(blo.x, blo.y), make_float2(-hi.x, -hi.y));
+    const float2 c = __fadd2_rn(make_float2(lo.z, lo.w), make_float2(-bhi.z, -bhi.w));
+    const float2 d = __fadd2_rn(make_float2(blo.z, blo.w), make_float2(-hi.z, -hi.w));
+    return fmaxf(fmaxf(fmaxf(fmaxf(a.x, a.y), fmaxf(b.x, b.y)), fmaxf(c.x, c.y)), fmaxf(d.x, d.y));
+#else
     const float a = fmaxf(fmaxf(lo.x - bhi.x, blo.x - hi.x), fmaxf(lo.y - bhi.y, blo.y - hi.y));
     const float b = fmaxf(fmaxf(lo.z - bhi.z, blo.z - hi.z), fmaxf(lo.w - bhi.w, blo.w - hi.w));
     return fmaxf(a, b);
+#endif
 }
 
 template <int Q>
@@ -327,8 +340,24 @@ struct Walker {
 template <int F0, int NC, int NP, int Q>
 __device__ __forceinline__ float point_box(const float2 (&nr)[NP], const Box<Q> &b) {
     float d = 0.0f;
+    constexpr int NPAIR = (F0 % 2 == 0) ? NC / 2 : 0;
+    // column pairs (box slots 2p, 2p+1 = columns F0 + 2p, F0 + 2p + 1) when the
+    // box slots line up with the packed reference pairs: lo - x and hi - x of
+    // two columns per FADD2 on adjacent registers (no operand moves), the
+    // same roundings as the per-column form below
 #pragma unroll
-    for (int g = 0; g < NC; ++g) {
+    for (int p = 0; p < NPAIR; ++p) {
+        const int g = 2 * p, c = F0 + g;
+        const float4 l4 = b.lo[g >> 2], h4 = b.hi[g >> 2];
+        const float2 l = (g & 3) == 0 ? make_float2(l4.x, l4.y) : make_float2(l4.z, l4.w);
+        const float2 h = (g & 3) == 0 ? make_float2(h4.x, h4.y) : make_float2(h4.z, h4.w);
+        const float2 el = __fadd2_rn(l, nr[c >> 1]);  // lo - x
+        const float2 eh = __fadd2_rn(h, nr[c >> 1]);  // hi - x
+        d = fmaxf(fmaxf(d, el.x), el.y);
+        d = fmaxf(fmaxf(d, -eh.x), -eh.y);
+    }
+#pragma unroll
+    for (int g = 2 * NPAIR; g < NC; ++g) {
         const int c = F0 + g;  // column
         const float x = (c & 1) ? nr[c >> 1].y : nr[c >> 1].x;  // -x_c
         const float4 l4 = b.lo[g >> 2], h4 = b.hi[g >> 2];
@@ -344,16 +373,31 @@ __device__ __forceinline__ float point_box(const float2 (&nr)[NP], const Box<Q> 
 // column g (the kNN-order boxes, columns 0 .. 4Q-1)
 template <int C0, int C1, int NP, int Q>
 __device__ __forceinline__ float point_box_cols(const float2 (&nr)[NP], const Box<Q> &b) {
+    // a leading odd column alone, then column pairs (two columns per FADD2,
+    // as in point_box), then a trailing odd column; bounds are constants
+    constexpr int P0 = (C0 + 1) & ~1, NPAIR = (C1 - P0) / 2, T0 = P0 + 2 * NPAIR;
     float d = 0.0f;
-#pragma unroll
-    for (int c = C0; c < C1; ++c) {
+    auto one = [&](int c) {
         const float x = (c & 1) ? nr[c >> 1].y : nr[c >> 1].x;  // -x_c
         const float4 l4 = b.lo[c >> 2], h4 = b.hi[c >> 2];
         const float l = (c & 3) == 0 ? l4.x : (c & 3) == 1 ? l4.y : (c & 3) == 2 ? l4.z : l4.w;
         const float h = (c & 3) == 0 ? h4.x : (c & 3) == 1 ? h4.y : (c & 3) == 2 ? h4.z : h4.w;
         const float2 e = __fadd2_rn(make_float2(l, h), make_float2(x, x));
         d = fmaxf(fmaxf(d, e.x), -e.y);
+    };
+    if constexpr (C0 < P0 && C0 < C1) one(C0);
+#pragma unroll
+    for (int p = 0; p < NPAIR; ++p) {
+        const int c = P0 + 2 * p;
+        const float4 l4 = b.lo[c >> 2], h4 = b.hi[c >> 2];
+        const float2 l = (c & 3) == 0 ? make_float2(l4.x, l4.y) : make_float2(l4.z, l4.w);
+        const float2 h = (c & 3) == 0 ? make_float2(h4.x, h4.y) : make_float2(h4.z, h4.w);
+        const float2 el = __fadd2_rn(l, nr[c >> 1]);
+        const float2 eh = __fadd2_rn(h, nr[c >> 1]);
+        d = fmaxf(fmaxf(d, el.x), el.y);
+        d = fmaxf(fmaxf(d, -eh.x), -eh.y);
     }
+    if constexpr (T0 < C1) one(T0);
     return d;
 }
 
@@ -617,7 +661,8 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) kn
 #pragma unroll
             for (int p = 0; p < NP; ++p) nr[p] = make_float2(-rr[p].x, -rr[p].y);
 #endif
-            need |= (thr > -INFINITY && (!prune || point_box<0, NBC, NP, kKnnQ>(nr, b) < thr)) ? (1u << r) : 0u;
+            // (a finished or padding reference has thr = -inf: no box distance is below it)
+            need |= (prune ? point_box<0, NBC, NP, kKnnQ>(nr, b) < thr : thr > -INFINITY) ? (1u << r) : 0u;
         }
         return need;
     };
@@ -1030,7 +1075,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
             float d;
             if constexpr (KO) d = point_box_cols<1, NBC, NP, Q>(gate_ref(r).v, b);
             else d = point_box<1, NG, NP, 1>(gate_ref(r).v, b);
-            need |= ((!prune && myhi[r] > -INFINITY) || d <= myhi[r]) ? (1u << r) : 0u;
+            need |= (prune ? d <= myhi[r] : myhi[r] > -INFINITY) ? (1u << r) : 0u;  // d >= 0
         }
         return need;
     };
