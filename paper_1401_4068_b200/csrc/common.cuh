@@ -33,6 +33,7 @@ struct ChunkInfo {
     double delta;   // |d32 - d64| bound (set by prep)
     int32_t ok32;   // fp32 filter usable for this chunk
     int32_t tile_lo;  // first sweep tile of this call's reference range (split searches)
+    int32_t sbg, sbk;  // float4 offsets of this chunk's block boxes in fbox / fboxk
 };
 
 struct TileRef {

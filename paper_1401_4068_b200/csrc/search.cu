@@ -432,6 +432,41 @@ __global__ void __launch_bounds__(T) sort_pca_kernel(
     for (int i = threadIdx.x; i < ci.n; i += T) perm[ci.row0 + i] = res[i];
 }
 
+// Block boxes: the union of each run of kBlockSubs sub-tile boxes of a chunk
+// (one warp per block), stored after the sub-tile boxes at the chunk's
+// ChunkInfo offset; the walkers test a whole block against their bound
+// before loading its sub-tile boxes.
+template <int Q>
+__global__ void __launch_bounds__(256) block_box_kernel(const ChunkInfo *__restrict__ info, int n_chunks,
+                                                        float4 *__restrict__ fbox, int knn) {
+    const int lane = threadIdx.x & 31;
+    const int blk = blockIdx.x * 8 + (threadIdx.x >> 5);
+    for (int cidx = blockIdx.y; cidx < n_chunks; cidx += gridDim.y) {
+        const ChunkInfo ci = info[cidx];
+        const int nsub = ci.npad / kSub;
+        if (!ci.ok32 || blk * kBlockSubs >= nsub) continue;
+        const int sub = blk * kBlockSubs + lane;
+        const float4 *fb = fbox + (ci.prow0 / kSub) * 2 * Q;
+        float4 *out = fbox + (knn ? ci.sbk : ci.sbg) + (int64_t)blk * 2 * Q;
+#pragma unroll
+        for (int h = 0; h < 2 * Q; ++h) {  // h < Q: lo quads, else hi quads
+            const bool lo = h < Q;
+            float4 v = lane < kBlockSubs && sub < nsub
+                           ? __ldg(fb + (int64_t)sub * 2 * Q + h)
+                           : (lo ? make_float4(INFINITY, INFINITY, INFINITY, INFINITY)
+                                 : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY));
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const float x = __shfl_xor_sync(0xffffffffu, v.x, off), y = __shfl_xor_sync(0xffffffffu, v.y, off);
+                const float z = __shfl_xor_sync(0xffffffffu, v.z, off), t = __shfl_xor_sync(0xffffffffu, v.w, off);
+                v = lo ? make_float4(fminf(v.x, x), fminf(v.y, y), fminf(v.z, z), fminf(v.w, t))
+                       : make_float4(fmaxf(v.x, x), fmaxf(v.y, y), fmaxf(v.z, z), fmaxf(v.w, t));
+            }
+            if (lane == 0) out[h] = v;
+        }
+    }
+}
+
 // kNN copy: fp32 rows in the kNN order + boxes over columns 0 .. 4*kKnnQ-1
 // (unused slots hold 0) + kmap (kNN position -> count-order position).
 // Runs after gather_kernel, which fills inv (row -> count-order position).
@@ -1038,6 +1073,13 @@ struct SearchWs {
     float *pts32k, *fboxk;
 };
 
+// block boxes (unions of kBlockSubs consecutive sub-tile boxes, Walker) follow
+// the sub-tile boxes in fbox / fboxk; chunk c's blocks start at block index
+// prow0 / (kBlockSubs * kSub) + c, so chunks never share one
+static int64_t block_boxes(const Plan &p, int n_chunks) {
+    return p.total_prows / ((int64_t)kBlockSubs * kSub) + n_chunks + 1;
+}
+
 static SearchWs layout_ws(Arena &a, const Plan &p, int n_chunks) {
     SearchWs w{};
     w.info = a.take<ChunkInfo>(n_chunks);
@@ -1047,7 +1089,7 @@ static SearchWs layout_ws(Arena &a, const Plan &p, int n_chunks) {
         w.stats = a.take<ColStats>(n_chunks);
         w.tile0 = a.take<int32_t>(2 * n_chunks + 1);
         w.pts32 = a.take<float>((size_t)p.total_prows * p.dp);
-        w.fbox = a.take<float>((size_t)(p.total_prows / kSub) * 2 * kGate);
+        w.fbox = a.take<float>((size_t)(p.total_prows / kSub + block_boxes(p, n_chunks)) * 2 * kGate);
         w.ka = a.take<uint32_t>(p.total_rows);
         w.kb = a.take<uint32_t>(p.total_rows);
         w.va = a.take<int32_t>(p.total_rows);
@@ -1066,9 +1108,28 @@ static SearchWs layout_ws(Arena &a, const Plan &p, int n_chunks) {
         w.kmap = a.take<int32_t>(p.total_rows);
         w.inv = a.take<int32_t>(p.total_rows);
         w.pts32k = a.take<float>((size_t)p.total_prows * p.dp);
-        w.fboxk = a.take<float>((size_t)(p.total_prows / kSub) * 2 * 4 * kKnnQ);
+        w.fboxk = a.take<float>((size_t)(p.total_prows / kSub + block_boxes(p, n_chunks)) * 2 * 4 * kKnnQ);
     }
     return w;
+}
+
+static int launch_block_boxes(cudaStream_t st, const Plan &p, const SearchWs &w, int n_chunks, bool gate,
+                              bool knn) {
+    const int nblk = (int)((p.max_npad / kSub + kBlockSubs - 1) / kBlockSubs);
+    dim3 grid((unsigned)((nblk + 7) / 8), (unsigned)std::min(n_chunks, 65535));
+    if (gate) {
+        ENTE_LAUNCH("block_box", st,
+                    block_box_kernel<1><<<grid, 256, 0, st>>>(w.info, n_chunks,
+                                                              reinterpret_cast<float4 *>(w.fbox), 0));
+        ENTE_CUDA(cudaGetLastError());
+    }
+    if (knn) {
+        ENTE_LAUNCH("block_box", st,
+                    block_box_kernel<kKnnQ><<<grid, 256, 0, st>>>(w.info, n_chunks,
+                                                                  reinterpret_cast<float4 *>(w.fboxk), 1));
+        ENTE_CUDA(cudaGetLastError());
+    }
+    return ENTE_OK;
 }
 
 static int num_sms() {
@@ -1198,7 +1259,9 @@ static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Pl
                                                              w.permk, w.inv, p.dp, w.pts32k,
                                                              w.fboxk, knn_only ? nullptr : w.kmap));
         ENTE_CUDA(cudaGetLastError());
-    return ENTE_OK;
+    // block boxes serve the shared-y m3 sweep only (BlockWalker); the other
+    // sweeps walk sub-tiles
+    return launch_block_boxes(st, p, w, n_chunks, false, knn_only);
 }
 
 // host chunk table + status (K_TOO_LARGE) + per-chunk first sweep tile
@@ -1220,6 +1283,11 @@ static int upload_chunks(cudaStream_t st, const ente_chunk *chunks, int n_chunks
         ci.delta = 0.0;
         ci.ok32 = 0;
         ci.tile_lo = 0;
+        {
+            const int64_t blk = ci.prow0 / ((int64_t)kBlockSubs * kSub) + c;
+            ci.sbg = (int32_t)((p.total_prows / kSub + blk) * 2);
+            ci.sbk = (int32_t)((p.total_prows / kSub + blk) * 2 * kKnnQ);
+        }
         prow += ci.npad;
         if (k > ci.n - 1) hstatus[c] = ENTE_CHUNK_K_TOO_LARGE;
         htile0[c] = ntiles;

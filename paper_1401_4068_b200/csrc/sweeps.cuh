@@ -62,6 +62,7 @@ __host__ __device__ constexpr int sweep_minb(int D, int cap) {
     return D <= 7 ? cap : (D <= 9 ? (cap < 28 ? cap : 28) : (D <= 11 ? (cap < 24 ? cap : 24)
                                                               : (D <= 13 ? (cap < 20 ? cap : 20) : 16)));
 }
+constexpr int kBlockSubs = 32;              // sub-tiles per walker block (one per lane)
 constexpr int kKnnQ = 2;                    // kNN sub-tile boxes: 4 * kKnnQ columns from 0
 
 
@@ -244,6 +245,89 @@ __device__ __forceinline__ float gap4(float4 lo, float4 hi, float4 blo, float4 b
 #endif
 }
 
+// Block walk over a chunk's sub-tiles in aligned blocks of kBlockSubs (= 32, one
+// per lane): the home block first, then blocks alternately above and below
+// it.  A block whose box (the union of its sub-tile boxes, block_box_kernel)
+// is not within the bound is skipped with one warp-uniform test; otherwise
+// every lane tests its sub-tile's box as before.  Every sub-tile is
+// considered once.  Used by the m3 count sweep, whose bounds (the bands)
+// are fixed: the order cannot change what is visited.  (The kNN passes keep the
+// sub-tile-outward Walker: there the visiting order decides how fast the
+// k-th distances shrink, and block order measured 34 % slower on C2.)
+template <int Q>
+struct BlockWalker {
+    int nsub, nwin, hb, w;
+    uint32_t mask;  // needed sub-tiles of the current block not yet issued
+    int wst;        // per lane: sub-tile of the current block (-1: none)
+    float wd;       // per lane: its box distance
+    Box<Q> own;     // the warp's own box, identical in all lanes
+    uint32_t need;  // per lane: refs_need() bits of the sub-tile last returned
+    int ln;         // this lane
+    const float4 *sb;  // this chunk's block boxes
+
+    __device__ void init(const float4 *__restrict__ fb, const float4 *__restrict__ sbox, int wrow, int n,
+                         int npad, int lane, int refs = kWarpRefs) {
+        ln = lane;
+        sb = sbox;
+        const int h0 = wrow / kSub;
+        const int nh = (min(wrow + refs, n) - wrow + kSub - 1) / kSub;
+        nsub = npad / kSub;
+        const int nblk = (nsub + kBlockSubs - 1) / kBlockSubs;
+        hb = h0 / kBlockSubs;
+        nwin = 1 + 2 * max(hb, nblk - 1 - hb);
+        w = -1;
+        mask = 0;
+        own = load_box<Q>(fb, h0);
+        for (int s = 1; s < nh; ++s) {
+            const Box<Q> b = load_box<Q>(fb, h0 + s);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                own.lo[q] = make_float4(fminf(own.lo[q].x, b.lo[q].x), fminf(own.lo[q].y, b.lo[q].y),
+                                        fminf(own.lo[q].z, b.lo[q].z), fminf(own.lo[q].w, b.lo[q].w));
+                own.hi[q] = make_float4(fmaxf(own.hi[q].x, b.hi[q].x), fmaxf(own.hi[q].y, b.hi[q].y),
+                                        fmaxf(own.hi[q].z, b.hi[q].z), fmaxf(own.hi[q].w, b.hi[q].w));
+            }
+        }
+    }
+
+    __device__ float dist(const Box<Q> &b) const {
+        float d = 0.0f;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) d = fmaxf(d, gap4(b.lo[q], b.hi[q], own.lo[q], own.hi[q]));
+        return d;
+    }
+
+    template <class RefTest>
+    __device__ int next(const float4 *__restrict__ fb, float bound, bool strict,
+                        RefTest &&refs_need) {
+        const int lane = ln;
+        for (;;) {
+            while (mask == 0) {
+                if (++w >= nwin) return -1;
+                const int k = (w + 1) >> 1;
+                const int blk = w == 0 ? hb : ((w & 1) ? hb + k : hb - k);
+                if (blk < 0 || blk * kBlockSubs >= nsub) continue;
+                const float bd = dist(load_box<Q>(sb, blk));  // warp-uniform
+                if (!(strict ? (bd < bound) : (bd <= bound))) continue;
+                const int st = blk * kBlockSubs + lane;
+                wst = st < nsub ? st : -1;
+                wd = wst >= 0 ? dist(load_box<Q>(fb, wst)) : INFINITY;
+                mask = __ballot_sync(0xffffffffu, wst >= 0 && (strict ? (wd < bound) : (wd <= bound)));
+            }
+            const int b = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const float d = __shfl_sync(0xffffffffu, wd, b);
+            if (!(strict ? (d < bound) : (d <= bound))) continue;  // the bound may have shrunk
+            const int st = __shfl_sync(0xffffffffu, wst, b);
+            const uint32_t nm = (uint32_t)refs_need(load_box<Q>(fb, st));
+            if (__any_sync(0xffffffffu, nm != 0u)) {
+                need = nm;
+                return st;
+            }
+        }
+    }
+};
+
 template <int Q>
 struct Walker {
     int h0, nh, nsub, npos;
@@ -269,8 +353,8 @@ struct Walker {
         if (nst >= 0) nb = load_box<Q>(fb, nst);
     }
 
-    __device__ void init(const float4 *__restrict__ fb, int wrow, int n, int npad, int lane,
-                         int refs = kWarpRefs) {
+    __device__ void init(const float4 *__restrict__ fb, const float4 *__restrict__, int wrow, int n,
+                         int npad, int lane, int refs = kWarpRefs) {
         ln = lane;
         h0 = wrow / kSub;
         nh = (min(wrow + refs, n) - wrow + kSub - 1) / kSub;
@@ -485,7 +569,7 @@ __global__ void __launch_bounds__(32, S > 16 ? 24 : (S > 8 ? 16 : sweep_minb(1 +
     fence_barrier_init();
     __syncwarp();
     Walker<kKnnQ> wk;
-    wk.init(fb, wrow, ci.n, ci.npad, lane);
+    wk.init(fb, reinterpret_cast<const float4 *>(fbox) + ci.sbk, wrow, ci.n, ci.npad, lane);
     float bound = INFINITY;  // warp max of the current k-th distances
     auto refs_need = [&](const Box<kKnnQ> &b) {
         bool need = !prune;
@@ -682,7 +766,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) kn
     fence_barrier_init();
     __syncwarp();
     Walker<kKnnQ> wk;
-    wk.init(fb, wrow, ci.n, ci.npad, lane);
+    wk.init(fb, reinterpret_cast<const float4 *>(fbox) + ci.sbk, wrow, ci.n, ci.npad, lane);
     float bound = INFINITY;  // warp max of the current k-th distances
     int slot_st = -1;
     uint32_t slot_need = 0u;
@@ -873,7 +957,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
     fence_barrier_init();
     __syncwarp();
     Walker<1> wk;
-    wk.init(fb, wrow, ci.n, ci.npad, lane);
+    wk.init(fb, reinterpret_cast<const float4 *>(fbox) + ci.sbg, wrow, ci.n, ci.npad, lane);
     int slot_st = -1;
     int issued = 0;
     uint32_t nsub = 0;
@@ -1082,8 +1166,13 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
     if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
     fence_barrier_init();
     __syncwarp();
-    Walker<Q> wk;
-    wk.init(fb, wrow, ci.n, ci.npad, lane, WR);
+    // m3 sweep over the kNN order: block walk (its kNN-order sub-tiles are
+    // scattered over m3 space, whole blocks fall outside the bands); the
+    // gate-column count passes keep the sub-tile walk (block boxes over
+    // four gate columns rarely exclude a block: C4 +0.4 %)
+    std::conditional_t<KO, BlockWalker<Q>, Walker<Q>> wk;
+    wk.init(fb, reinterpret_cast<const float4 *>(fbox) + (Q == 1 ? ci.sbg : ci.sbk), wrow, ci.n, ci.npad,
+            lane, WR);
     if constexpr (KO) {  // column 0 is not an m3 column: the warp box spans it
         wk.own.lo[0].x = -INFINITY;
         wk.own.hi[0].x = INFINITY;
