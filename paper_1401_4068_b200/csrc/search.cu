@@ -1259,9 +1259,9 @@ static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Pl
                                                              w.permk, w.inv, p.dp, w.pts32k,
                                                              w.fboxk, knn_only ? nullptr : w.kmap));
         ENTE_CUDA(cudaGetLastError());
-    // block boxes serve the shared-y m3 sweep only (BlockWalker); the other
-    // sweeps walk sub-tiles
-    return launch_block_boxes(st, p, w, n_chunks, false, knn_only);
+    // kNN-order block boxes: the kNN passes' KnnWalker and the shared-y m3
+    // sweep's BlockWalker (the gate-column count passes walk sub-tiles)
+    return launch_block_boxes(st, p, w, n_chunks, false, true);
 }
 
 // host chunk table + status (K_TOO_LARGE) + per-chunk first sweep tile

@@ -417,6 +417,72 @@ struct Walker {
     }
 };
 
+#ifndef ENTE_KNN_WA
+#define ENTE_KNN_WA 2
+#endif
+
+// kNN walk: the sub-tile-outward Walker for its first ENTE_KNN_WA windows
+// (the nearest Morton neighbours, which shrink the k-th distances fast),
+// then the block walk of BlockWalker over the rest of the chunk, skipping
+// the sub-tiles already visited.
+template <int Q>
+struct KnnWalker : Walker<Q> {
+    int w;  // block window (-2: still in the sub-tile phase)
+    const float4 *sb;
+
+    __device__ void init(const float4 *__restrict__ fb, const float4 *__restrict__ sbox, int wrow, int n,
+                         int npad, int lane, int refs = kWarpRefs) {
+        Walker<Q>::init(fb, sbox, wrow, n, npad, lane, refs);
+        this->npos = min(this->npos, 32 * ENTE_KNN_WA);
+        w = -2;
+        sb = sbox;
+    }
+
+    template <class RefTest>
+    __device__ int next(const float4 *__restrict__ fb, float bound, bool strict,
+                        RefTest &&refs_need) {
+        const int h0 = this->h0, nh = this->nh, nsub = this->nsub;
+        if (w == -2) {
+            const int st = Walker<Q>::next(fb, bound, strict, refs_need);
+            if (st >= 0 || nh + 2 * max(h0, nsub - h0 - nh) <= this->npos) return st;
+            w = -1;
+            this->mask = 0;
+        }
+        // sub-tiles the first phase visited: [vlo, vhi]
+        const int pa = this->npos - nh;
+        const int vlo = h0 - (pa + 1) / 2, vhi = h0 + nh - 1 + pa / 2;
+        const int hb = h0 / kBlockSubs, nblk = (nsub + kBlockSubs - 1) / kBlockSubs;
+        const int nwin = 1 + 2 * max(hb, nblk - 1 - hb);
+        const int lane = this->ln;
+        for (;;) {
+            while (this->mask == 0) {
+                if (++w >= nwin) return -1;
+                const int k = (w + 1) >> 1;
+                const int blk = w == 0 ? hb : ((w & 1) ? hb + k : hb - k);
+                if (blk < 0 || blk * kBlockSubs >= nsub) continue;
+                if (blk * kBlockSubs >= vlo && blk * kBlockSubs + kBlockSubs - 1 <= vhi) continue;
+                const float bd = this->dist(load_box<Q>(sb, blk));  // warp-uniform
+                if (!(strict ? (bd < bound) : (bd <= bound))) continue;
+                const int st = blk * kBlockSubs + lane;
+                this->wst = (st < nsub && (st < vlo || st > vhi)) ? st : -1;
+                this->wd = this->wst >= 0 ? this->dist(load_box<Q>(fb, this->wst)) : INFINITY;
+                this->mask = __ballot_sync(0xffffffffu, this->wst >= 0 &&
+                                                            (strict ? (this->wd < bound) : (this->wd <= bound)));
+            }
+            const int b = __ffs(this->mask) - 1;
+            this->mask &= this->mask - 1;
+            const float d = __shfl_sync(0xffffffffu, this->wd, b);
+            if (!(strict ? (d < bound) : (d <= bound))) continue;
+            const int st = __shfl_sync(0xffffffffu, this->wst, b);
+            const uint32_t nm = (uint32_t)refs_need(load_box<Q>(fb, st));
+            if (__any_sync(0xffffffffu, nm != 0u)) {
+                this->need = nm;
+                return st;
+            }
+        }
+    }
+};
+
 // fp32 distance from a reference (negated packed coordinates) to a sub-tile
 // box over the columns F0 .. F0 + NC - 1 (box slot g = column - F0): a lower
 // bound of the reference's fp32 distance to every row of the sub-tile over
@@ -568,7 +634,7 @@ __global__ void __launch_bounds__(32, S > 16 ? 24 : (S > 8 ? 16 : sweep_minb(1 +
     if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
     fence_barrier_init();
     __syncwarp();
-    Walker<kKnnQ> wk;
+    KnnWalker<kKnnQ> wk;
     wk.init(fb, reinterpret_cast<const float4 *>(fbox) + ci.sbk, wrow, ci.n, ci.npad, lane);
     float bound = INFINITY;  // warp max of the current k-th distances
     auto refs_need = [&](const Box<kKnnQ> &b) {
@@ -765,7 +831,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_KNN_MINB)) kn
     if (lane < NSLOT) mbar_init(&ring.full[lane], 1);
     fence_barrier_init();
     __syncwarp();
-    Walker<kKnnQ> wk;
+    KnnWalker<kKnnQ> wk;
     wk.init(fb, reinterpret_cast<const float4 *>(fbox) + ci.sbk, wrow, ci.n, ci.npad, lane);
     float bound = INFINITY;  // warp max of the current k-th distances
     int slot_st = -1;
