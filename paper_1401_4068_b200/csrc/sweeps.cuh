@@ -527,13 +527,12 @@ __device__ __forceinline__ float point_box_cols(const float2 (&nr)[NP], const Bo
     // as in point_box), then a trailing odd column; bounds are constants
     constexpr int P0 = (C0 + 1) & ~1, NPAIR = (C1 - P0) / 2, T0 = P0 + 2 * NPAIR;
     float d = 0.0f;
-    auto one = [&](int c) {
+    auto one = [&](int c) {  // (scalar adds: a packed one would need its operands moved)
         const float x = (c & 1) ? nr[c >> 1].y : nr[c >> 1].x;  // -x_c
         const float4 l4 = b.lo[c >> 2], h4 = b.hi[c >> 2];
         const float l = (c & 3) == 0 ? l4.x : (c & 3) == 1 ? l4.y : (c & 3) == 2 ? l4.z : l4.w;
         const float h = (c & 3) == 0 ? h4.x : (c & 3) == 1 ? h4.y : (c & 3) == 2 ? h4.z : h4.w;
-        const float2 e = __fadd2_rn(make_float2(l, h), make_float2(x, x));
-        d = fmaxf(fmaxf(d, e.x), -e.y);
+        d = fmaxf(fmaxf(d, __fadd_rn(l, x)), -__fadd_rn(h, x));
     };
     if constexpr (C0 < P0 && C0 < C1) one(C0);
 #pragma unroll
@@ -1196,7 +1195,9 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
         rs.lo[ri] = b.lo;
         rs.hi[ri] = b.hi;
         rs.w[ri] = b.w;
-        myhi[r] = b.hi;
+        // the reference box test's threshold: the band's upper end, or (no
+        // pruning) +inf for a live reference and -inf for padding (d >= 0)
+        myhi[r] = prune ? b.hi : (b.hi > -INFINITY ? INFINITY : -INFINITY);
         rs.cnt[0][ri] = rs.cnt[1][ri] = rs.cnt[2][ri] = 0u;
         rs.nev[ri] = 0;
     }
@@ -1225,7 +1226,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
             float d;
             if constexpr (KO) d = point_box_cols<1, NBC, NP, Q>(gate_ref(r).v, b);
             else d = point_box<1, NG, NP, 1>(gate_ref(r).v, b);
-            need |= (prune ? d <= myhi[r] : myhi[r] > -INFINITY) ? (1u << r) : 0u;  // d >= 0
+            need |= d <= myhi[r] ? (1u << r) : 0u;
         }
         return need;
     };
