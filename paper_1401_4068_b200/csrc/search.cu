@@ -1261,7 +1261,8 @@ static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Pl
         ENTE_CUDA(cudaGetLastError());
     // kNN-order block boxes: the kNN passes' KnnWalker and the shared-y m3
     // sweep's BlockWalker (the gate-column count passes walk sub-tiles)
-    return launch_block_boxes(st, p, w, n_chunks, false, true);
+    // (chunks of <= 32 sub-tiles never leave the KnnWalker's sub-tile phase)
+    return launch_block_boxes(st, p, w, n_chunks, false, knn_only || p.max_npad / kSub > kBlockSubs);
 }
 
 // host chunk table + status (K_TOO_LARGE) + per-chunk first sweep tile
