@@ -45,10 +45,10 @@ constexpr int kGate = 4;                    // gate columns in the Morton key an
 #define ENTE_CNT_UNROLL 2    // count pass: row-pair iterations unrolled per loop trip
 #endif
 #ifndef ENTE_KNNC_UNROLL
-#define ENTE_KNNC_UNROLL 1   // compacted kNN pass: row-pair iterations per loop trip
+#define ENTE_KNNC_UNROLL 2   // compacted kNN pass: row-pair iterations per loop trip
 #endif
 #ifndef ENTE_KO_RT
-#define ENTE_KO_RT 3  // references per lane of the shared-y m3/joint sweep (96-reference groups)
+#define ENTE_KO_RT 2  // references per lane of the shared-y m3/joint sweep (64-reference groups)
 #endif
 #ifndef ENTE_CNT_MINB
 #define ENTE_CNT_MINB 32
