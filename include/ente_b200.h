@@ -288,6 +288,13 @@ int ente_seed_states(const uint32_t *words, const int64_t *offsets, int64_t n_it
                      uint64_t *out);
 int ente_draw_permutations(const uint32_t *words, const int64_t *offsets, int64_t n_perms,
                            int reps, int strict, int32_t *out);
+/* ente_seed_states_cols -- ente_seed_states for the entropy lists
+ * prefix + (cols[0][i], ..., cols[n_cols-1][i]) (each value one uint32 word,
+ * 0 <= v < 2^32; n_prefix + n_cols <= 16): the tuple seeds
+ * SeedSequence((seed, u, 0|idx+1)) of every jitter stream without building
+ * a word list per item.  cols [host] n_cols x n_items int64, row-major. */
+int ente_seed_states_cols(const uint32_t *prefix, int n_prefix, const int64_t *cols, int n_cols,
+                          int64_t n_items, uint64_t *out);
 
 /* ente_host_gather -- multi-threaded concatenation of n host buffers
  * (srcs[i], bytes[i]) into dst (pinned staging for one H2D copy of a batch).

@@ -70,6 +70,7 @@ def _declare(L):
         "ente_microbench_pce": ([i32, i32, ctypes.POINTER(dbl), vp], i32),
         "ente_search_work": ([ctypes.POINTER(ctypes.c_ulonglong)] * 2, None),
         "ente_seed_states": ([u32p, ctypes.POINTER(i64), i64, u64p], i32),
+        "ente_seed_states_cols": ([u32p, i32, ctypes.POINTER(i64), i32, i64, u64p], i32),
         "ente_host_gather": ([ctypes.POINTER(vp), ctypes.POINTER(i64), i64, vp], i32),
         "ente_draw_permutations": ([u32p, ctypes.POINTER(i64), i64, i32, i32, i32p], i32),
     }

@@ -162,6 +162,36 @@ int ente_seed_states(const uint32_t *words, const int64_t *offsets, int64_t n_it
     return ENTE_OK;
 }
 
+int ente_seed_states_cols(const uint32_t *prefix, int n_prefix, const int64_t *cols, int n_cols,
+                          int64_t n_items, uint64_t *out) {
+    if (n_items < 0 || n_prefix < 0 || n_cols < 0 || n_prefix + n_cols > 16 || n_prefix + n_cols < 1 ||
+        (n_items > 0 && (!out || (n_prefix && !prefix) || (n_cols && !cols)))) {
+        ente::set_error("ente_seed_states_cols: bad arguments");
+        return ENTE_ERR_ARG;
+    }
+    for (int64_t j = 0; j < (int64_t)n_cols * n_items; ++j)
+        if (cols[j] < 0 || cols[j] > 0xffffffffll) {
+            ente::set_error("ente_seed_states_cols: column value outside one uint32 word");
+            return ENTE_ERR_ARG;
+        }
+    ente::parallel_for(n_items, 8192, [&](int64_t lo, int64_t hi) {
+        uint32_t ent[16];
+        for (int j = 0; j < n_prefix; ++j) ent[j] = prefix[j];
+        for (int64_t i = lo; i < hi; ++i) {
+            for (int j = 0; j < n_cols; ++j) ent[n_prefix + j] = (uint32_t)cols[(int64_t)j * n_items + i];
+            uint64_t s[4];
+            seed_sequence_state(ent, n_prefix + n_cols, s);
+            Pcg64 g;
+            g.seed(s);
+            out[4 * i + 0] = (uint64_t)(g.state >> 64);
+            out[4 * i + 1] = (uint64_t)g.state;
+            out[4 * i + 2] = (uint64_t)(g.inc >> 64);
+            out[4 * i + 3] = (uint64_t)g.inc;
+        }
+    });
+    return ENTE_OK;
+}
+
 int ente_draw_permutations(const uint32_t *words, const int64_t *offsets, int64_t n_perms,
                            int reps, int strict, int32_t *out) {
     if (n_perms < 0 || reps < 0 || (n_perms > 0 && (!words || !offsets || !out))) {

@@ -108,7 +108,7 @@ def search_path(dim: int, masks, k: int) -> int:
 # device-level entry points (tensors in, tensors out; used by ksg / bench)
 # ---------------------------------------------------------------------------
 def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int, reuse: bool = False,
-                  tag: str = "", split=None, split_fill=(0.0, 0)):
+                  tag: str = "", split=None, split_fill=(0.0, 0), table=None):
     """ente_search on a device-resident [rows, dim] fp64 matrix.
 
     Returns (eps [rows] f64, counts [n_marg, rows] int32, status [n_chunks] int32),
@@ -119,7 +119,8 @@ def search_device(pts64: torch.Tensor, rows0, ns, masks, k: int, reuse: bool = F
         raise TypeError("pts64 must be a contiguous CUDA float64 tensor")
     rows, dim = pts64.shape
     L = nat.lib()
-    table = nat.chunk_table(rows0, ns)
+    if table is None:  # (callers running several stages on one batch pass theirs)
+        table = nat.chunk_table(rows0, ns)
     marr = nat.masks_array(masks)
     if reuse:
         eps = nat.scratch("search.eps" + tag, (rows,), torch.float64)
@@ -162,11 +163,12 @@ class SharedY:
 
 
 def search_te_shared_device(pts64: torch.Tensor, rows0, ns, d_y: int, k: int, shared: SharedY,
-                            tag: str = ""):
+                            tag: str = "", table=None):
     """ente_search_te_shared on device-resident TE chunks: (eps, counts [3, rows], status)."""
     rows, dim = pts64.shape
     L = nat.lib()
-    table = nat.chunk_table(rows0, ns)
+    if table is None:
+        table = nat.chunk_table(rows0, ns)
     eps = nat.scratch("search.eps" + tag, (rows,), torch.float64)
     counts = nat.scratch("search.counts" + tag, (3, rows), torch.int32)
     status = nat.scratch("search.status" + tag, (max(1, len(ns)),), torch.int32)

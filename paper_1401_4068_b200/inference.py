@@ -279,7 +279,6 @@ class PairPipeline:
         n = len(it)
         nsub = 1 if n < 2 * MIN_SUB_BATCH else min(SUB_BATCHES, n // MIN_SUB_BATCH)
         bounds = np.linspace(0, n, nsub + 1).astype(int)
-        states = self._states(it)
         main = torch.cuda.current_stream()
         streams = _streams(min(2, nsub))
         outs = []
@@ -288,14 +287,14 @@ class PairPipeline:
             stream = streams[b % len(streams)]
             stream.wait_stream(main)
             with torch.cuda.stream(stream):
-                outs.append(self._sub(it[lo:hi], states[lo:hi], f".s{b % len(streams)}"))
+                outs.append(self._sub(it[lo:hi], f".s{b % len(streams)}"))
         for stream in streams:
             main.wait_stream(stream)
         te = torch.cat([t for t, _ in outs]).cpu().numpy()
         st = torch.cat([s for _, s in outs]).cpu().numpy()
         return te, st
 
-    def _sub(self, it: np.ndarray, states: np.ndarray, tag: str):
+    def _sub(self, it: np.ndarray, tag: str):
         L = nat.lib()
         n = len(it)
         pts = nat.scratch("pipe.joint" + tag, (n * self.m, self.dim), torch.float64)
@@ -306,6 +305,7 @@ class PairPipeline:
                                        it.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_int32)),
                                        n, perms_ptr, nat.ptr(pts), nat.stream_handle()),
                   "ente_pack_te_items")
+        states = self._states(it)  # host work while the device packs
         rows0 = np.arange(n, dtype=np.int64) * self.m
         ns = np.full(n, self.m, dtype=np.int64)
         shared = None

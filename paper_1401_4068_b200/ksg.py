@@ -59,13 +59,15 @@ class _PsiTable:
 _PSI = _PsiTable()
 
 
-def te_reduce_device(counts: torch.Tensor, rows0, ns, k: int, tag: str = "") -> torch.Tensor:
-    """ente_te_reduce over a [3, rows] int32 device count matrix; returns [n_chunks] f64."""
+def te_reduce_device(counts: torch.Tensor, rows0, ns, k: int, tag: str = "", table=None) -> torch.Tensor:
+    """ente_te_reduce over a [3, rows] int32 device count matrix; returns [n_chunks] f64.
+    table: nat.chunk_table(rows0, ns) when the caller has it."""
     L = nat.lib()
     rows = counts.shape[1]
     psi = _PSI.get(int(np.max(ns)) + 2)
     out = torch.empty(len(ns), dtype=torch.float64, device=counts.device)
-    table = nat.chunk_table(rows0, ns)
+    if table is None:
+        table = nat.chunk_table(rows0, ns)
     ws = nat.workspace(L.ente_te_reduce_workspace_size(table, len(ns)), tag)
     nat.check(L.ente_te_reduce(nat.ptr(counts), rows, table, len(ns), nat.ptr(psi), psi.numel(),
                                float(special.digamma(k)), nat.ptr(out), nat.ptr(ws), ws.numel(),
@@ -87,11 +89,12 @@ def te_from_counts(counts: TermCounts) -> float:
 
 
 def jitter_device(pts64: torch.Tensor, rows0, ns, amplitude: float, seeds,
-                  tag: str = "") -> torch.Tensor:
+                  tag: str = "", table=None) -> torch.Tensor:
     """ente_jitter in place on a device [rows, dim] matrix; returns the status tensor."""
     L = nat.lib()
     dim = pts64.shape[1]
-    table = nat.chunk_table(rows0, ns)
+    if table is None:
+        table = nat.chunk_table(rows0, ns)
     states = None
     if amplitude > 0:
         if isinstance(seeds, np.ndarray) and seeds.dtype == np.uint64:
@@ -126,16 +129,18 @@ def te_chunks_device(pts64: torch.Tensor, rows0, ns, d_y: int, d_x: int, k: int,
     come back as device tensors; the caller reads status before using te
     (a failed chunk's TE is meaningless).  `tag` selects per-stream scratch.
     """
-    status = jitter_device(pts64, rows0, ns, amplitude, seeds, tag)
+    table = nat.chunk_table(rows0, ns)  # one host chunk table for every stage
+    status = jitter_device(pts64, rows0, ns, amplitude, seeds, tag, table)
     if sync:
         st = status.cpu().numpy()
         if (st != 0).any():
             return None, st
     if shared is not None:  # every chunk pools the same target rows: y marginals once per point
-        _, counts, _ = search_te_shared_device(pts64, rows0, ns, d_y, k, shared, tag=tag)
+        _, counts, _ = search_te_shared_device(pts64, rows0, ns, d_y, k, shared, tag=tag, table=table)
     else:
-        _, counts, _ = search_device(pts64, rows0, ns, te_masks(d_y, d_x), k, reuse=True, tag=tag)
-    te = te_reduce_device(counts, rows0, ns, k, tag)
+        _, counts, _ = search_device(pts64, rows0, ns, te_masks(d_y, d_x), k, reuse=True, tag=tag,
+                                     table=table)
+    te = te_reduce_device(counts, rows0, ns, k, tag, table)
     return (te, st) if sync else (te, status)
 
 

@@ -128,7 +128,25 @@ def jitter_states(master_seed, us, stream_ids) -> np.ndarray:
     """PCG64 (state_hi, state_lo, inc_hi, inc_lo) of
     default_rng(SeedSequence((master_seed, u, stream_id))) per item, [n, 4] uint64
     (stream_id = 0 for the original data, idx + 1 for surrogate idx)."""
-    return _states_from_words(*_tuple_words(master_seed, us, stream_ids))
+    prefix = _coerce(master_seed)
+    if prefix is None:
+        raise TypeError(f"seed must be an int or a sequence of ints, got {master_seed!r}")
+    cols = np.stack([np.asarray(us, dtype=np.int64).reshape(-1),
+                     np.asarray(stream_ids, dtype=np.int64).reshape(-1)])
+    n = cols.shape[1]
+    out = np.empty((n, 4), dtype=np.uint64)
+    if n == 0:
+        return out
+    if (cols < 0).any():
+        raise ValueError("expected non-negative integer")
+    if int(cols.max()) > _MASK32 or len(prefix) + 2 > 16:  # multi-word values: per-item word lists
+        return _states_from_words(*_tuple_words(master_seed, us, stream_ids))
+    pre = np.asarray(prefix, dtype=np.uint32)
+    nat.check(nat.lib().ente_seed_states_cols(
+        pre.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), len(pre),
+        cols.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 2, n,
+        out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))), "ente_seed_states_cols")
+    return out
 
 
 def pcg_states(seeds) -> np.ndarray:
