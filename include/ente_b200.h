@@ -209,6 +209,9 @@ int ente_search_te_shared(const double *pts64, int64_t total_rows, int dim, cons
  *                       inc_lo} = np.random.PCG64(seed).state before any draw
  *   amplitude           jitter amplitude; <= 0 skips the jitter but still
  *                       runs the checks
+ * Batches of >= 4096 chunks with one n at row0 = base + c*n copy pcg_state
+ * as given (then the chunk table is built on the device): pass pinned memory
+ * to keep the host free, and keep it unchanged until the stream has run. 
  * ------------------------------------------------------------------------- */
 int ente_jitter(double *pts64, int dim, const ente_chunk *chunks, int n_chunks,
                 const uint64_t *pcg_state, double amplitude, int32_t *status, void *workspace,

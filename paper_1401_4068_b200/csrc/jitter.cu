@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(32) jitter_std_kernel(const double *__restrict
 // Threads own elements e0 + t + kJitThreads * i (coalesced); each advances
 // its state by kJitThreads steps with one precomputed affine LCG jump.
 constexpr int kJitPerThread = 64;
+constexpr int kJitUniformMin = 4096;  // smaller batches: the host table is cheap
 
 template <int kJitThreads>
 __global__ void __launch_bounds__(kJitThreads) jitter_apply_kernel(double *__restrict__ pts, int dim,
@@ -253,13 +254,33 @@ __global__ void __launch_bounds__(T) check_kernel(const double *__restrict__ pts
 struct JitWs {
     JitChunk *ch;
     double *hw;
+    uint64_t *raw;  // PCG64 states as given (uniform batches)
 };
 
 static JitWs jit_layout(Arena &a, int n_chunks) {
     JitWs w;
     w.ch = a.take<JitChunk>(n_chunks);
     w.hw = a.take<double>((size_t)n_chunks * kMaxDim);
+    w.raw = a.take<uint64_t>((size_t)n_chunks * 4);
     return w;
+}
+
+// uniform batches (chunk c = rows [row0 + c*n, +n)): the chunk table is built
+// on the device from the PCG64 states copied as they are -- from pinned
+// memory that copy does not hold the host, unlike a pageable multi-MB table
+__global__ void __launch_bounds__(256) jit_uniform_kernel(JitChunk *__restrict__ ch,
+                                                          const uint64_t *__restrict__ raw, int n_chunks,
+                                                          int64_t row0, int n, int have_states) {
+    for (int c = blockIdx.x * 256 + threadIdx.x; c < n_chunks; c += gridDim.x * 256) {
+        JitChunk j{};
+        j.row0 = row0 + (int64_t)c * n;
+        j.n = n;
+        if (have_states) {
+            j.state = {raw[4 * c + 0], raw[4 * c + 1]};
+            j.inc = {raw[4 * c + 2], raw[4 * c + 3]};
+        }
+        ch[c] = j;
+    }
 }
 
 }  // namespace ente
@@ -291,9 +312,24 @@ extern "C" int ente_jitter(double *pts64, int dim, const ente_chunk *chunks, int
         set_error("ente_jitter: workspace of %zu bytes too small (need %zu)", ws_bytes, a.used);
         return ENTE_ERR_WORKSPACE;
     }
-    std::vector<JitChunk> h(n_chunks);
-    int max_n = 0;
-    for (int c = 0; c < n_chunks; ++c) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    bool uniform = n_chunks >= kJitUniformMin;
+    for (int c = 1; c < n_chunks && uniform; ++c)
+        uniform = chunks[c].n == chunks[0].n && chunks[c].row0 == chunks[0].row0 + (int64_t)c * chunks[0].n;
+    if (uniform && chunks[0].n < 1) uniform = false;
+    std::vector<JitChunk> h(uniform ? 0 : n_chunks);
+    int max_n = uniform ? chunks[0].n : 0;
+    if (uniform) {
+        if (pcg_state)
+            ENTE_CUDA(cudaMemcpyAsync(w.raw, pcg_state, sizeof(uint64_t) * 4 * (size_t)n_chunks,
+                                      cudaMemcpyHostToDevice, st));
+        const unsigned blocks = (unsigned)std::min(1024, (n_chunks + 255) / 256);
+        ENTE_LAUNCH("jitter_table", st,
+                    jit_uniform_kernel<<<blocks, 256, 0, st>>>(w.ch, w.raw, n_chunks, chunks[0].row0,
+                                                               chunks[0].n, pcg_state ? 1 : 0));
+        ENTE_CUDA(cudaGetLastError());
+    }
+    for (int c = 0; c < n_chunks && !uniform; ++c) {
         if (chunks[c].n < 1) {
             set_error("ente_jitter: chunk %d has n=%d", c, chunks[c].n);
             return ENTE_ERR_ARG;
@@ -306,8 +342,8 @@ extern "C" int ente_jitter(double *pts64, int dim, const ente_chunk *chunks, int
         }
         max_n = max_n > chunks[c].n ? max_n : chunks[c].n;
     }
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    ENTE_CUDA(cudaMemcpyAsync(w.ch, h.data(), sizeof(JitChunk) * n_chunks, cudaMemcpyHostToDevice, st));
+    if (!uniform)
+        ENTE_CUDA(cudaMemcpyAsync(w.ch, h.data(), sizeof(JitChunk) * n_chunks, cudaMemcpyHostToDevice, st));
     if (amplitude > 0) {
         if (dim <= 8)
             ENTE_LAUNCH("jitter_std", st,

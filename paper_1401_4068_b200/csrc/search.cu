@@ -1265,11 +1265,76 @@ static int launch_orders(cudaStream_t st, const double *pts64, int dim, const Pl
     return launch_block_boxes(st, p, w, n_chunks, false, knn_only || p.max_npad / kSub > kBlockSubs);
 }
 
-// host chunk table + status (K_TOO_LARGE) + per-chunk first sweep tile
+// Uniform batches (every chunk n rows at row0 = base + c*n, no split: the TE
+// pipeline's case) get their chunk table, status and tile map written on the
+// device from a few scalars: no multi-MB host tables, and no pageable copy
+// that would hold the host until the stream reaches it.
+constexpr int kUniformMinChunks = 4096;  // smaller batches: host tables are cheap
+
+struct UniformChunks {
+    int64_t row0, stride, total_subs;
+    int32_t n, npad, tiles, status;
+};
+
+__global__ void __launch_bounds__(256) uniform_chunks_kernel(UniformChunks u, int n_chunks,
+                                                             ChunkInfo *__restrict__ info,
+                                                             int32_t *__restrict__ status,
+                                                             int32_t *__restrict__ tile0) {
+    for (int c = blockIdx.x * 256 + threadIdx.x; c <= n_chunks; c += gridDim.x * 256) {
+        if (c == n_chunks) {
+            tile0[n_chunks] = n_chunks * u.tiles;
+            continue;
+        }
+        ChunkInfo ci{};
+        ci.row0 = u.row0 + (int64_t)c * u.stride;
+        ci.n = u.n;
+        ci.npad = u.npad;
+        ci.prow0 = (int64_t)c * u.npad;
+        ci.delta = 0.0;
+        ci.ok32 = 0;
+        ci.tile_lo = 0;
+        const int64_t blk = ci.prow0 / ((int64_t)kBlockSubs * kSub) + c;
+        ci.sbg = (int32_t)((u.total_subs + blk) * 2);
+        ci.sbk = (int32_t)((u.total_subs + blk) * 2 * kKnnQ);
+        info[c] = ci;
+        status[c] = u.status;
+        tile0[c] = c * u.tiles;
+        tile0[n_chunks + 1 + c] = 0;
+    }
+}
+
+// host chunk table + status (K_TOO_LARGE) + per-chunk first sweep tile;
+// htile0 comes back empty when the tile map was written on the device
 static int upload_chunks(cudaStream_t st, const ente_chunk *chunks, int n_chunks, int k,
                          const Plan &p, const SearchWs &w, int32_t *status,
                          std::vector<int32_t> &htile0, int32_t &ntiles, int split_index = 0,
                          int split_count = 1) {
+    if (split_count == 1 && n_chunks >= kUniformMinChunks && w.tile0) {
+        const int32_t n0 = chunks[0].n;
+        const int64_t base = chunks[0].row0;
+        bool uniform = true;
+        for (int c = 1; c < n_chunks && uniform; ++c)
+            uniform = chunks[c].n == n0 && chunks[c].row0 == base + (int64_t)c * n0;
+        if (uniform) {
+            UniformChunks u;
+            u.row0 = base;
+            u.stride = n0;
+            u.n = n0;
+            u.npad = (int32_t)round_up(n0, kTJ);
+            u.total_subs = p.total_prows / kSub;
+            u.status = k > n0 - 1 ? ENTE_CHUNK_K_TOO_LARGE : ENTE_CHUNK_OK;
+            u.tiles = (p.fast && u.status == ENTE_CHUNK_OK) ? (n0 + kWarpRefs - 1) / kWarpRefs : 0;
+            ntiles = n_chunks * u.tiles;
+            htile0.clear();
+            const unsigned blocks = (unsigned)std::min<int64_t>((n_chunks + 256) / 256, 1024);
+            ENTE_LAUNCH("uniform_chunks", st,
+                        uniform_chunks_kernel<<<blocks, 256, 0, st>>>(u, n_chunks, w.info, status, w.tile0));
+            ENTE_CUDA(cudaGetLastError());
+            ENTE_CUDA(cudaMemsetAsync(w.ovf_n, 0, 2 * sizeof(int32_t), st));
+            if (w.rs_flag) ENTE_CUDA(cudaMemsetAsync(w.rs_flag, 0, sizeof(int32_t) * n_chunks, st));
+            return ENTE_OK;
+        }
+    }
     std::vector<ChunkInfo> hinfo(n_chunks);
     std::vector<int32_t> hstatus(n_chunks, ENTE_CHUNK_OK);
     htile0.assign(2 * n_chunks + 1, 0);
@@ -1514,8 +1579,9 @@ static int radius_fast(const double *pts64, int64_t total_rows, int dim, const e
     int32_t ntiles = 0;
     int rc = upload_chunks(st, chunks, n_chunks, 1, p, w, status, htile0, ntiles);
     if (rc != ENTE_OK) return rc;
-    ENTE_CUDA(cudaMemcpyAsync(w.tile0, htile0.data(), sizeof(int32_t) * (2 * n_chunks + 1),
-                              cudaMemcpyHostToDevice, st));
+    if (!htile0.empty())
+        ENTE_CUDA(cudaMemcpyAsync(w.tile0, htile0.data(), sizeof(int32_t) * (2 * n_chunks + 1),
+                                  cudaMemcpyHostToDevice, st));
     {
         const int64_t elems = p.total_rows * dd;
         const unsigned blocks = (unsigned)std::min<int64_t>((elems + 255) / 256, (int64_t)num_sms() * 32);
@@ -1627,8 +1693,9 @@ static int search_impl(const double *pts64, int64_t total_rows, int dim, const e
         // kNN pass covers exactly the references its count pass needs
         rc = launch_orders(st, pts64, dim, p, w, n_chunks, status, prune, split_count == 1);
         if (rc != ENTE_OK) return rc;
-        ENTE_CUDA(cudaMemcpyAsync(w.tile0, htile0.data(), sizeof(int32_t) * (2 * n_chunks + 1),
-                                  cudaMemcpyHostToDevice, st));
+        if (!htile0.empty())
+            ENTE_CUDA(cudaMemcpyAsync(w.tile0, htile0.data(), sizeof(int32_t) * (2 * n_chunks + 1),
+                                      cudaMemcpyHostToDevice, st));
         const unsigned nt = (unsigned)ntiles;
         const KnnFn knn_fn = knn_table(p.dy, p.dx, p.slots, p.max_npad);
         const CountFn count_fn = count_table(p.dy, p.dx, p.max_npad);
@@ -1819,8 +1886,9 @@ extern "C" int ente_search_te_shared(const double *pts64, int64_t total_rows, in
     }
     rc = launch_orders(st, pts64, dim, p, w_, n_chunks, status, prune, 1, false, true);
     if (rc != ENTE_OK) return rc;
-    ENTE_CUDA(cudaMemcpyAsync(w_.tile0, htile0.data(), sizeof(int32_t) * (2 * n_chunks + 1),
-                              cudaMemcpyHostToDevice, st));
+    if (!htile0.empty())
+        ENTE_CUDA(cudaMemcpyAsync(w_.tile0, htile0.data(), sizeof(int32_t) * (2 * n_chunks + 1),
+                                  cudaMemcpyHostToDevice, st));
     ENTE_CUDA(cudaMemcpyAsync(b.chunk_perm, chunk_perm, sizeof(int32_t) * n_chunks,
                               cudaMemcpyHostToDevice, st));
     SweepSet ss;

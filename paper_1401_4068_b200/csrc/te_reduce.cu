@@ -139,11 +139,13 @@ template <int T>
 __global__ void __launch_bounds__(T) te_reduce_kernel(
     const int32_t *__restrict__ counts, int64_t total_rows, const RedChunk *__restrict__ chunks,
     const double *__restrict__ psi, int64_t table_len, double psi_k, uint64_t *__restrict__ ka,
-    uint64_t *__restrict__ kb, double *__restrict__ out_te) {
+    uint64_t *__restrict__ kb, double *__restrict__ out_te, RedChunk uniform) {
     __shared__ SortSmemT<T> sm;
     __shared__ int bad;
     __shared__ int n_leaves;
-    const RedChunk ch = chunks[blockIdx.x];
+    // (uniform batches: chunk c at uniform.row0 + c * uniform.n, no table)
+    const RedChunk ch = chunks ? chunks[blockIdx.x]
+                               : RedChunk{uniform.row0 + (int64_t)blockIdx.x * uniform.n, uniform.n, 0};
     const int n = ch.n;
     constexpr bool SMS = T == kSortThreadsSmall;  // small segments sort in shared memory
     __shared__ uint64_t skey[SMS ? 2 : 1][SMS ? kSortSmallN : 1];
@@ -237,12 +239,20 @@ extern "C" int ente_te_reduce(const int32_t *counts, int64_t total_rows, const e
         return ENTE_ERR_WORKSPACE;
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    ENTE_CUDA(cudaMemcpyAsync(dch, h.data(), sizeof(RedChunk) * n_chunks, cudaMemcpyHostToDevice, st));
+    // uniform batches pass two scalars instead of the table (a pageable copy of
+    // a few MB would hold the host until the stream reached it)
+    bool uniform = n_chunks > 1;
+    for (int c = 1; c < n_chunks && uniform; ++c)
+        uniform = h[c].n == h[0].n && h[c].row0 == h[0].row0 + (int64_t)c * h[0].n;
+    const RedChunk uni{h[0].row0, h[0].n, 0};
+    if (!uniform)
+        ENTE_CUDA(cudaMemcpyAsync(dch, h.data(), sizeof(RedChunk) * n_chunks, cudaMemcpyHostToDevice, st));
     ENTE_LAUNCH("te_reduce", st,
                 (max_n <= kSortSmallN ? te_reduce_kernel<kSortThreadsSmall> : te_reduce_kernel<kSortThreads>)
-                <<<n_chunks, max_n <= kSortSmallN ? kSortThreadsSmall : kSortThreads, 0, st>>>(counts, total_rows, dch,
+                <<<n_chunks, max_n <= kSortSmallN ? kSortThreadsSmall : kSortThreads, 0, st>>>(counts, total_rows,
+                                                                  uniform ? nullptr : dch,
                                                                   psi_table, table_len, psi_k, ka,
-                                                                  kb, out_te));
+                                                                  kb, out_te, uni));
     ENTE_CUDA(cudaGetLastError());
     return ENTE_OK;
 }

@@ -152,6 +152,7 @@ class PairPipeline:
     def __init__(self, source, target, spec_x, spec_y, config: AnalysisConfig,
                  x_device=None, y_device=None):
         self.cfg = config
+        self._pinned_keep = []  # pinned jitter-state buffers of the wave in flight
         self.sx, self.sy = spec_x, spec_y
         self.reps, self.n_samples = target.values.shape
         self.t_lo, self.t_hi = config.window
@@ -267,9 +268,14 @@ class PairPipeline:
 
     def _states(self, it: np.ndarray) -> np.ndarray:
         """Jitter PCG64 states per item: SeedSequence((seed, u, 0 | idx + 1)), independent
-        of the window (inference.py:148, 171-172)."""
-        return np.ascontiguousarray(seeds.jitter_states(self.cfg.seed, it[:, 0],
-                                                        it[:, 1].astype(np.int64) + 1))
+        of the window (inference.py:148, 171-172).  Written to pinned memory, so
+        ente_jitter's copy of them does not hold the host; the buffer is kept
+        until the wave has been read back (_wave clears the list)."""
+        buf = torch.empty((len(it), 4), dtype=torch.int64, pin_memory=True)
+        out = buf.numpy().view(np.uint64)
+        seeds.jitter_states(self.cfg.seed, it[:, 0], it[:, 1].astype(np.int64) + 1, out=out)
+        self._pinned_keep.append(buf)
+        return out
 
     def _wave(self, it: np.ndarray):
         """One device batch, split into sub-batches alternating over two CUDA
@@ -277,6 +283,7 @@ class PairPipeline:
         sorts, gathers, reduction) overlap another's compute-bound sweeps.
         Returns (te, status), read once at the end."""
         n = len(it)
+        self._pinned_keep = []  # the previous wave was read back: its staging is free
         nsub = 1 if n < 2 * MIN_SUB_BATCH else min(SUB_BATCHES, n // MIN_SUB_BATCH)
         bounds = np.linspace(0, n, nsub + 1).astype(int)
         main = torch.cuda.current_stream()

@@ -124,23 +124,28 @@ def _states_from_words(words, offsets) -> np.ndarray:
     return out
 
 
-def jitter_states(master_seed, us, stream_ids) -> np.ndarray:
+def jitter_states(master_seed, us, stream_ids, out=None) -> np.ndarray:
     """PCG64 (state_hi, state_lo, inc_hi, inc_lo) of
     default_rng(SeedSequence((master_seed, u, stream_id))) per item, [n, 4] uint64
-    (stream_id = 0 for the original data, idx + 1 for surrogate idx)."""
+    (stream_id = 0 for the original data, idx + 1 for surrogate idx).
+    out: a C-contiguous [n, 4] uint64 array to fill (e.g. pinned memory)."""
     prefix = _coerce(master_seed)
     if prefix is None:
         raise TypeError(f"seed must be an int or a sequence of ints, got {master_seed!r}")
     cols = np.stack([np.asarray(us, dtype=np.int64).reshape(-1),
                      np.asarray(stream_ids, dtype=np.int64).reshape(-1)])
     n = cols.shape[1]
-    out = np.empty((n, 4), dtype=np.uint64)
+    if out is None:
+        out = np.empty((n, 4), dtype=np.uint64)
+    elif out.shape != (n, 4) or out.dtype != np.uint64 or not out.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous [n, 4] uint64 array")
     if n == 0:
         return out
     if (cols < 0).any():
         raise ValueError("expected non-negative integer")
     if int(cols.max()) > _MASK32 or len(prefix) + 2 > 16:  # multi-word values: per-item word lists
-        return _states_from_words(*_tuple_words(master_seed, us, stream_ids))
+        out[...] = _states_from_words(*_tuple_words(master_seed, us, stream_ids))
+        return out
     pre = np.asarray(prefix, dtype=np.uint32)
     nat.check(nat.lib().ente_seed_states_cols(
         pre.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), len(pre),
