@@ -334,3 +334,20 @@ def test_large_k_shared_memory_lists(k):
         e, c = oracle.search(pts, margs, k)
         assert np.array_equal(r.kth_distance, e)
         assert all(np.array_equal(a, b) for a, b in zip(r.radius_counts, c))
+
+
+def test_uniform_batch_search_equals_host_table_path():
+    """5000 equal chunks (device-built chunk table) give the results of the
+    same chunks with one ragged chunk appended (host-built table)."""
+    rng = np.random.default_rng(21)
+    chunks = [Chunk(rng.standard_normal((64, 5))) for _ in range(5000)]
+    margs = cases.te_margs(2, 2)
+    uni = batch_search([(c, margs) for c in chunks], 4)
+    mixed = batch_search([(c, margs) for c in chunks] + [(Chunk(rng.standard_normal((65, 5))), margs)], 4)
+    for a, b in zip(uni, mixed):
+        assert np.array_equal(a.kth_distance, b.kth_distance)
+        assert all(np.array_equal(x, y) for x, y in zip(a.radius_counts, b.radius_counts))
+    for i in (0, 2500, 4999):
+        eps, cnts = oracle.search(chunks[i].points, margs, 4)
+        assert np.array_equal(uni[i].kth_distance, eps)
+        assert all(np.array_equal(x, y) for x, y in zip(uni[i].radius_counts, cnts))

@@ -190,3 +190,27 @@ def test_te_reduce_runs_of_equal_high_key_bits():
     nat.check(L.ente_te_reduce(nat.ptr(counts), m, tab, 1, nat.ptr(psi), psi.numel(), 0.25,
                                nat.ptr(out), nat.ptr(ws), ws.numel(), nat.stream_handle()), "reduce")
     assert float(out.cpu()[0]) == float(ref)
+
+
+def test_uniform_batch_tables_built_on_device():
+    """>= 4096 equal chunks take the device-built chunk tables (search, jitter
+    from pinned states, reduction): the same TE as per-window calls on the
+    host-table path and as the CPU oracle."""
+    import dataclasses
+    from paper_1401_4068_b200 import analyze_windows
+    wl = workloads.CONFIGS["C4"]
+    xv, yv = wl.ensembles()
+    xv, yv = xv[:60], yv[:60]
+    spec = EmbeddingSpec(*wl.spec)
+    cfg = AnalysisConfig(u_candidates=(8, 10), window=(501, 501), k=4, n_surrogates=20, seed=5)
+    X, Y = EnsembleSeries("X", xv), EnsembleSeries("Y", yv)
+    starts = list(range(501, 501 + 110))  # 110 windows x 42 chunks = 4620 chunks in one wave
+    batch = analyze_windows(X, Y, spec, spec, cfg, starts)
+    for i in (0, 57, 109):
+        one = analyze_pair(X, Y, spec, spec, dataclasses.replace(cfg, window=(starts[i], starts[i])))
+        assert batch[i].te_curve == one.te_curve
+        assert batch[i].surrogate_values.tolist() == one.surrogate_values.tolist()
+    ref = oracle.analyze_pair(xv, yv, wl.spec, wl.spec, (8, 10), (starts[57], starts[57]), k=4,
+                              n_surrogates=20, seed=5)
+    assert batch[57].te_value == ref["te_value"]
+    assert batch[57].surrogate_values.tolist() == list(ref["surrogate_values"])
