@@ -1781,9 +1781,12 @@ struct SyBufs {
     double *ys, *box;
 };
 
-static size_t sy_smem_bytes(int C, int nsub) {
-    return (size_t)C * 4 * 3 + 2 * (size_t)(C + 1) * 4 + 2 * (size_t)C * 4 + (size_t)nsub * 4 +
-           (size_t)kSyBins * 2;
+static bool sy_pack(int64_t m) { return m < 65536; }  // counters fit 16-bit halves
+
+static size_t sy_smem_bytes(int C, int nsub, bool pack) {
+    const int halves = pack ? 1 : 2;
+    return (size_t)C * 4 * 3 + halves * (size_t)(C + 1) * 4 + halves * (size_t)C * 4 +
+           (size_t)nsub * 4 + (size_t)kSyBins * 2;
 }
 
 static SyBufs sy_layout(Arena &a, int64_t m, int C, int dd) {
@@ -1813,7 +1816,7 @@ static bool sy_usable(const Plan &p, int n_chunks, int64_t m, int k) {
     return p.fast && p.lay.nout == 3 && p.lay.slot[0] == 0 && p.lay.slot[1] == 1 && p.lay.slot[2] == 2 &&
            p.max_npad >= kCompactMinRows && k + 1 <= 16 && find_sweep_set(p.dy, p.dx, ss) &&
            ss.count3 != nullptr && 1 + p.dy <= kSyMaxY && n_chunks < 65535 &&
-           sy_smem_bytes(n_chunks, (int)((m + 31) / 32)) <= 200 * 1024;
+           sy_smem_bytes(n_chunks, (int)((m + 31) / 32), sy_pack(m)) <= 200 * 1024;
 }
 
 static void te_masks_of(int dy, int dim, uint32_t *masks) {
@@ -1965,11 +1968,12 @@ extern "C" int ente_search_te_shared(const double *pts64, int64_t total_rows, in
     ENTE_LAUNCH("sy_gather", st,
                 sy_gather_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(y0, g, b.yperm, b.ys, b.box));
     ENTE_CUDA(cudaGetLastError());
-    const size_t smem = sy_smem_bytes(n_chunks, g.nsub);
-    ENTE_CUDA(cudaFuncSetAttribute(sy_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+    const bool pack = sy_pack(m);
+    const size_t smem = sy_smem_bytes(n_chunks, g.nsub, pack);
+    auto kern = pack ? sy_count_kernel<true> : sy_count_kernel<false>;
+    ENTE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ENTE_LAUNCH("sy_count", st,
-                sy_count_kernel<<<(unsigned)m, kSyThreads, smem, st>>>(
+                kern<<<(unsigned)m, kSyThreads, smem, st>>>(
                     y0, b.ys, b.yperm, b.box, g, b.ka, b.kb, b.va, b.vb, b.qs, b.parity, w_.info, b.chunk_perm,
                     inv_perms, pts64, dim, out_eps, total_rows, out_counts));
     ENTE_CUDA(cudaGetLastError());

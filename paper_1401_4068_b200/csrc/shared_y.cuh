@@ -35,7 +35,10 @@ namespace ente {
 #define ENTE_SY_THREADS 256
 #endif
 constexpr int kSyThreads = ENTE_SY_THREADS;
-constexpr int kSyQueue = 1024;  // pending exact checks per CTA (shared memory)
+#ifndef ENTE_SY_QUEUE
+#define ENTE_SY_QUEUE 512
+#endif
+constexpr int kSyQueue = ENTE_SY_QUEUE;  // pending exact checks per CTA (shared memory)
 constexpr int kSyMaxY = 9;  // y columns (1 + d_y), d_y <= 8
 
 struct SyGeom {
@@ -175,7 +178,10 @@ __global__ void __launch_bounds__(256) sy_gather_kernel(const double *__restrict
     }
 }
 
-constexpr int kSyBins = 4096;  // lookup table over each point's radius range (uint16 entries)
+#ifndef ENTE_SY_BINS
+#define ENTE_SY_BINS 2048
+#endif
+constexpr int kSyBins = ENTE_SY_BINS;  // lookup table over each point's radius range (uint16 entries)
 
 __device__ __forceinline__ double sy_radius(uint32_t key) {  // truncated radius r' of a key
     return __longlong_as_double((long long)((uint64_t)key << 32));
@@ -202,6 +208,11 @@ __device__ __forceinline__ int sy_upper(const uint32_t *key, const uint16_t *tab
 // counts q for certain when r'_k > D0 + M, never when r'_k < (D0 - M)(1 -
 // 2^-19), and otherwise (rare: |r - D0| within M + 2^-20 r) q is settled on
 // the jittered rows with the exact radius eps_c.
+// PACK (m < 2^16 shared points): the two marginals' counters share one
+// 32-bit word per query (y-past low half, y_t + y-past high half), and the
+// exact additions likewise, so the CTA's shared memory drops by 16 B per
+// query and four CTAs fit an SM instead of three.
+template <bool PACK>
 __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
     const double *__restrict__ y0, const double *__restrict__ ys, const int32_t *__restrict__ yperm,
     const double *__restrict__ box, SyGeom g, const uint32_t *__restrict__ ka,
@@ -214,11 +225,28 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
     const int C = g.C;
     uint32_t *key = reinterpret_cast<uint32_t *>(sy_smem);
     int32_t *cid = reinterpret_cast<int32_t *>(key + C);
-    int32_t *dA = cid + C;       // C + 1 difference counters (y-past)
-    int32_t *d2 = dA + C + 1;    // C + 1 (y_t + y-past)
-    int32_t *xA = d2 + C + 1;    // C exact additions
-    int32_t *x2 = xA + C;
+    int32_t *dA = cid + C;                    // C + 1 difference counters (y-past)
+    int32_t *d2 = PACK ? dA : dA + C + 1;     // C + 1 (y_t + y-past)
+    int32_t *xA = d2 + C + 1;                 // C exact additions
+    int32_t *x2 = PACK ? xA : xA + C;
     uint32_t *qsm = reinterpret_cast<uint32_t *>(x2 + C);  // k-th neighbour records (C)
+    // counter updates and reads (PACK: halves of one word)
+    auto add_d = [&](int u, int which) {
+        if constexpr (PACK) atomicAdd(reinterpret_cast<uint32_t *>(&dA[u]), which ? 0x10000u : 1u);
+        else atomicAdd(which ? &d2[u] : &dA[u], 1);
+    };
+    auto add_x = [&](int k, int which) {
+        if constexpr (PACK) atomicAdd(reinterpret_cast<uint32_t *>(&xA[k]), which ? 0x10000u : 1u);
+        else atomicAdd(which ? &x2[k] : &xA[k], 1);
+    };
+    auto get = [&](const int32_t *lo, const int32_t *hi, int k, int which) -> int {
+        if constexpr (PACK) {
+            const uint32_t v = (uint32_t)lo[k];
+            return which ? (int)(v >> 16) : (int)(v & 0xFFFFu);
+        } else {
+            return which ? hi[k] : lo[k];
+        }
+    };
     int32_t *list = reinterpret_cast<int32_t *>(qsm + C);  // queued subtiles (nsub)
     uint16_t *tab = reinterpret_cast<uint16_t *>(list + g.nsub);  // kSyBins
     __shared__ int nlist, wq_n[kSyThreads / 32];
@@ -234,9 +262,13 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
         key[k] = keys[k];
         cid[k] = vals[k];
         qsm[k] = qs[off + vals[k]];
-        xA[k] = x2[k] = 0;
+        xA[k] = 0;
+        x2[k] = 0;
     }
-    for (int k = tid; k <= C; k += kSyThreads) dA[k] = d2[k] = 0;
+    for (int k = tid; k <= C; k += kSyThreads) {
+        dA[k] = 0;
+        d2[k] = 0;
+    }
     if (tid == 0) nlist = 0;
     if (tid < kSyThreads / 32) wq_n[tid] = 0;
     double yp[kSyMaxY];
@@ -292,7 +324,7 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
         const double *rq = pts64 + row_in(c, q / g.w, q - (q / g.w) * g.w) * dim;
         double dd = 0.0;
         for (int col = which ? 0 : 1; col < g.dd; ++col) dd = fmax(dd, fabs(__dsub_rn(rp[col], rq[col])));
-        if (dd < eps[ip]) atomicAdd(which ? &x2[k] : &xA[k], 1);
+        if (dd < eps[ip]) add_x(k, which);
     };
     auto drain = [&]() {  // warp-uniform
         __syncwarp();
@@ -314,14 +346,14 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
                 const double d0 = which ? b2 : a;
                 if (d0 - g.margin > rmax) continue;  // outside every query
                 const int u = sy_upper(key, tab, C, r0, inv_bw, d0 + g.margin);
-                if (u < C) atomicAdd(which ? &d2[u] : &dA[u], 1);
+                if (u < C) add_d(u, which);
                 // near the radius (r' >= (d0 - M)(1 - 2^-19)): exact, queued
                 const double lo_x = (d0 - g.margin) * (1.0 - 0x1p-19);
                 for (int k = u - 1; k >= 0 && sy_radius(key[k]) >= lo_x; --k) {
                     const uint32_t ks = qsm[k];
                     if ((ks & 0x3FFFFFFFu) == (uint32_t)q) {  // the k-th neighbour itself:
                         // its marginal distance is <= eps, equal unless resolve saw it below
-                        if ((ks >> (30 + which)) & 1u) atomicAdd(which ? &x2[k] : &xA[k], 1);
+                        if ((ks >> (30 + which)) & 1u) add_x(k, which);
                         continue;
                     }
                     const int slot = atomicAdd(&wq_n[warp], 1);
@@ -345,8 +377,8 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
     const int per = (C + NW - 1) / NW, k0 = warp * per, k1 = min(C, k0 + per);
     int sA = 0, s2 = 0;
     for (int k = k0 + lane; k < k1; k += 32) {
-        sA += dA[k];
-        s2 += d2[k];
+        sA += get(dA, d2, k, 0);
+        s2 += get(dA, d2, k, 1);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -365,7 +397,7 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
     }
     for (int base = k0; base < k1; base += 32) {
         const int k = base + lane;
-        int vA = k < k1 ? dA[k] : 0, v2 = k < k1 ? d2[k] : 0;
+        int vA = k < k1 ? get(dA, d2, k, 0) : 0, v2 = k < k1 ? get(dA, d2, k, 1) : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int tA = __shfl_up_sync(0xffffffffu, vA, o), t2 = __shfl_up_sync(0xffffffffu, v2, o);
@@ -377,8 +409,8 @@ __global__ void __launch_bounds__(kSyThreads) sy_count_kernel(
         if (k < k1) {
             const int c = cid[k];
             const int64_t row = row_in(c, pr, pt);
-            out_counts[row] = runA + vA + xA[k];
-            out_counts[total_rows + row] = run2 + v2 + x2[k];
+            out_counts[row] = runA + vA + get(xA, x2, k, 0);
+            out_counts[total_rows + row] = run2 + v2 + get(xA, x2, k, 1);
         }
         runA += __shfl_sync(0xffffffffu, vA, 31);
         run2 += __shfl_sync(0xffffffffu, v2, 31);
