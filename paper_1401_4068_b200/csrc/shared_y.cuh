@@ -36,7 +36,7 @@ namespace ente {
 #endif
 constexpr int kSyThreads = ENTE_SY_THREADS;
 #ifndef ENTE_SY_QUEUE
-#define ENTE_SY_QUEUE 512
+#define ENTE_SY_QUEUE 1024
 #endif
 constexpr int kSyQueue = ENTE_SY_QUEUE;  // pending exact checks per CTA (shared memory)
 constexpr int kSyMaxY = 9;  // y columns (1 + d_y), d_y <= 8
