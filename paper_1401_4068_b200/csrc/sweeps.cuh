@@ -44,6 +44,9 @@ constexpr int kGate = 4;                    // gate columns in the Morton key an
 #ifndef ENTE_CNT_UNROLL
 #define ENTE_CNT_UNROLL 2    // count pass: row-pair iterations unrolled per loop trip
 #endif
+#ifndef ENTE_KO_UNROLL
+#define ENTE_KO_UNROLL 1     // m3 sweep: row-pair iterations unrolled per loop trip
+#endif
 #ifndef ENTE_KNNC_UNROLL
 #define ENTE_KNNC_UNROLL 2   // compacted kNN pass: row-pair iterations per loop trip
 #endif
@@ -1352,7 +1355,7 @@ __global__ void __launch_bounds__(32, sweep_minb(1 + DY + DX, ENTE_CNT_MINB)) co
 #pragma unroll
             for (int q = 0; q < NQ; ++q) ra[q] = pr[q];
             // (KO rows are cheaper: two rows per loop trip measured 4 % faster)
-            constexpr int kTrip = KO ? 1 : ENTE_CNT_UNROLL;
+            constexpr int kTrip = KO ? ENTE_KO_UNROLL : ENTE_CNT_UNROLL;
 #pragma unroll kTrip
             for (int s = 0; s < STEPS; s += 2, pr += 2 * STRIDE) {
 #pragma unroll
